@@ -1,0 +1,476 @@
+#!/usr/bin/env python
+"""Benchmark of the ℓFEM numeric assembly hot path on B200 (BASELINE.json metric:
+elements/s and CSR nnz/s of fp64 mass+stiffness numeric assembly, % HBM
+roofline, 1/2/4/8 GPU).
+
+One "step" = one lfem_assemble_numeric call producing every kind the config
+names (C5: M, A, A_a) over the whole mesh (all ranks together), inputs
+resident in HBM.  The one-time symbolic phase is timed and reported
+separately (`symbolic_ms`).  Multi-GPU: one process per GPU (torchrun),
+contiguous row blocks of the SFC-ordered mesh, halo elements duplicated,
+no collective in the numeric phase; time = max over ranks (CUDA events).
+
+  python bench.py [--gpus N --steps K --warmup W --config C5]
+  python bench.py --impl reference ...   (the CPU oracle arm, rank 0 only)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+L2_BYTES = 126 * 2 ** 20
+KIND_BITS = {"M": 1, "A": 2, "Aa": 4}
+KIND_INDEX = {"M": 0, "A": 1, "Aa": 2}
+CONFIG_DESC = {
+    "C1": "P1 icosphere L3 (1,280 tri), radial noise 1e-3, M+A, TRI3_DEG2",
+    "C2": "P2 icosphere L7 (327,680 curved tri), M+A, TRI6_DEG4",
+    "C3": "P1 perturbed icosphere L9 (5,242,880 tri), M+A_a, u updated per step, TRI3_DEG2",
+    "C4": "P2 Kuhn cube 96^3x6 (5,308,416 tets), displaced, M+A, TET11_DEG4",
+    "C5": "P2 icosphere L10 (20,971,520 curved tri, 41,943,042 nodes), SFC order, M+A+A_a, TRI6_DEG4",
+}
+FLOP_PER_ELEM = {"C1": 120, "C2": 1780, "C3": 120, "C4": 9600, "C5": 2640}  # SURVEY §8(d).3 model
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def algorithmic_bytes(name, n_elems, nref, n_nodes, nnz, kinds, has_coeff):
+    """BASELINE.json: connectivity + coordinates (each node once) + CSR values
+    written once; + the coefficient u (one read per node) for C3/C5."""
+    b = n_elems * nref * 4 + n_nodes * 24 + len(kinds) * nnz * 8
+    if has_coeff:
+        b += n_nodes * 8
+    return b
+
+
+def build_mesh(name):
+    import lfem_inputs as li
+    t0 = time.time()
+    m = li.make_config(name)
+    return m, time.time() - t0
+
+
+def partition_rows(conn, n_nodes, world):
+    """Contiguous row blocks balanced by incident (element, local row) counts."""
+    if world == 1:
+        return [0, n_nodes]
+    w = np.bincount(conn.ravel(), minlength=n_nodes).astype(np.int64)
+    c = np.cumsum(w)
+    tot = int(c[-1])
+    bounds = [0]
+    for r in range(1, world):
+        bounds.append(int(np.searchsorted(c, tot * r / world)))
+    bounds.append(n_nodes)
+    return bounds
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- oracle (CPU) legs
+def oracle_sample(m, kinds, coeff, target_s):
+    """Time the oracle as it stands on a contiguous block of rows sized for
+    about target_s seconds; returns (elements/s equivalent, rows, seconds, threads)."""
+    import oracle
+    nt = os.cpu_count() or 1
+    rows0 = min(m.n_nodes, 20000)
+    t0 = time.perf_counter()
+    oracle.assemble_rows(m, kinds, rows=np.arange(rows0, dtype=np.int64), coeff=coeff, nthreads=nt)
+    dt0 = time.perf_counter() - t0
+    rows = int(min(m.n_nodes, max(rows0, rows0 * target_s / max(dt0, 1e-3))))
+    t0 = time.perf_counter()
+    c = oracle.assemble_rows(m, kinds, rows=np.arange(rows, dtype=np.int64), coeff=coeff, nthreads=nt)
+    dt = time.perf_counter() - t0
+    equiv_elems = m.n_elems * rows / m.n_nodes
+    return equiv_elems / dt, rows, dt, nt, c.nnz
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    name = args.config
+    m, gen_s = build_mesh(name)
+    kinds = m.extra["kinds"]
+    coeff = m.coeff
+    import oracle
+    nt = os.cpu_count() or 1
+    # calibrate, then size each step for ~budget/(K+W) seconds
+    budget = float(os.environ.get("LFEM_REF_BUDGET_S", "90"))
+    rows0 = min(m.n_nodes, 20000)
+    t0 = time.perf_counter()
+    oracle.assemble_rows(m, kinds, rows=np.arange(rows0, dtype=np.int64), coeff=coeff, nthreads=nt)
+    dt0 = time.perf_counter() - t0
+    per_step = budget / max(1, args.steps + args.warmup)
+    rows = int(min(m.n_nodes, max(2000, rows0 * per_step / max(dt0, 1e-3))))
+    times = []
+    for it in range(args.warmup + args.steps):
+        r0 = (it * rows) % max(1, m.n_nodes - rows + 1)
+        rr = np.arange(r0, r0 + rows, dtype=np.int64)
+        t0 = time.perf_counter()
+        oracle.assemble_rows(m, kinds, rows=rr, coeff=coeff, nthreads=nt)
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times)
+    equiv = m.n_elems * rows / m.n_nodes * len(times)
+    value = equiv / t
+    line = {"impl": "reference", "metric": "elements/s (fp64 numeric assembly, all kinds of the config)",
+            "value": value, "unit": "elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / len(times), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, lfem_inputs)",
+            "config": {"workload": f"{name}: {CONFIG_DESC[name]}", "kinds": list(kinds)},
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": nt, "kind": "oracle",
+                             "sample": f"{rows} contiguous rows per step of {m.n_nodes} "
+                                       f"(elements/s = n_elems * rows/n_rows / t); per-step sample"},
+            "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_lfem(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_14035_b200 import lfem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    name = args.config
+
+    # ---- inputs: rank 0 generates (seeded), broadcast over NCCL (plumbing, untimed)
+    gen_s = 0.0
+    if rank == 0:
+        m, gen_s = build_mesh(name)
+        meta = torch.tensor([m.n_nodes, m.n_elems, m.nref, m.domain, m.order, m.quad,
+                             1 if m.coeff is not None else 0], dtype=torch.int64, device=dev)
+    else:
+        m = None
+        meta = torch.empty(7, dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.broadcast(meta, 0)
+    n_nodes, n_elems, nref, domain, order, quad, has_coeff = [int(x) for x in meta.tolist()]
+    if rank == 0:
+        coords = torch.as_tensor(m.coords).to(dev)
+        conn = torch.as_tensor(m.conn).to(dev)
+        coeff = torch.as_tensor(m.coeff).to(dev) if has_coeff else None
+        kinds = tuple(m.extra["kinds"])
+        extra_uB = torch.as_tensor(m.extra["uB"]).to(dev) if "uB" in m.extra else None
+    else:
+        coords = torch.empty((n_nodes, 3), dtype=torch.float64, device=dev)
+        conn = torch.empty((n_elems, nref), dtype=torch.int32, device=dev)
+        coeff = torch.empty(n_nodes, dtype=torch.float64, device=dev) if has_coeff else None
+        kinds = None
+        extra_uB = torch.empty(n_nodes, dtype=torch.float64, device=dev) if name == "C3" else None
+    if world > 1:
+        dist.broadcast(coords, 0)
+        dist.broadcast(conn, 0)
+        if coeff is not None:
+            dist.broadcast(coeff, 0)
+        if extra_uB is not None:
+            dist.broadcast(extra_uB, 0)
+        obj = [kinds]
+        dist.broadcast_object_list(obj, 0)
+        kinds = obj[0]
+    kmask = sum(KIND_BITS[k] for k in kinds)
+
+    # ---- partition + symbolic (one-time, timed separately)
+    conn_np = conn.cpu().numpy() if world > 1 else None
+    bounds = partition_rows(conn_np, n_nodes, world) if world > 1 else [0, n_nodes]
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    stream = torch.cuda.current_stream()
+    mesh = lfem.lfem_mesh_create(domain, order, quad, coords, conn)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    plan = lfem.lfem_assemble_symbolic(mesh, r0, r1)
+    torch.cuda.synchronize()
+    symbolic_ms = 1e3 * (time.perf_counter() - t0)
+    variant = {"auto": lfem.LFEM_NUMERIC_AUTO, "v0": lfem.LFEM_NUMERIC_V0, "tiled": lfem.LFEM_NUMERIC_TILED}[args.variant]
+    lfem.lfem_plan_set_variant(plan, variant)
+    vals = [None, None, None]
+    for k in kinds:
+        vals[KIND_INDEX[k]] = torch.empty(plan.nnz, dtype=torch.float64, device=dev)
+
+    # C3: u(t) = cos(2 pi t/100) uA + sin(2 pi t/100) uB (reading G12) by lfem_axpby each step
+    u_work = torch.empty_like(coeff) if (name == "C3" and coeff is not None) else None
+
+    def step(t):
+        cf = coeff
+        if u_work is not None:
+            th = 2 * math.pi * (t % 100) / 100
+            lfem.lfem_axpby(math.cos(th), coeff, math.sin(th), extra_uB, u_work)
+            cf = u_work
+        lfem.lfem_assemble_numeric(plan, kmask, cf, vals)
+
+    # global sizes
+    tot = torch.tensor([plan.nnz, plan.n_elems_local], dtype=torch.int64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot)
+    nnz_total, elems_local_total = int(tot[0]), int(tot[1])
+    alg_bytes_rank = algorithmic_bytes(name, plan.n_elems_local, nref, plan.n_rows, plan.nnz, kinds, has_coeff)
+    alg_bytes_total = algorithmic_bytes(name, n_elems, nref, n_nodes, nnz_total, kinds, has_coeff)
+    flush = alg_bytes_rank < 4 * L2_BYTES
+    flush_buf = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
+
+    for t in range(args.warmup):
+        step(t)
+    lfem.lfem_plan_check(plan)
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    # ---- timed region (device time, max over ranks)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if flush:
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for t in range(args.steps):
+            flush_buf.zero_()
+            ev[t][0].record(stream)
+            step(t)
+            ev[t][1].record(stream)
+        torch.cuda.synchronize()
+        elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
+    else:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(args.steps):
+            step(t)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        elapsed_ms = e0.elapsed_time(e1)
+    if world > 1:
+        dist.barrier()
+    lfem.lfem_plan_check(plan)
+    # per-kernel profile pass (same launches, CUDA events around each kernel)
+    lfem.lfem_profile_enable(plan, True)
+    nprof = max(3, min(args.steps, 20))
+    for t in range(nprof):
+        if flush:
+            flush_buf.zero_()
+        step(t)
+    prof = lfem.lfem_profile_read(plan)
+    lfem.lfem_profile_enable(plan, False)
+    clk = clocks.stop()
+
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tmax)
+    ms_per_step = elapsed_ms / args.steps
+    value = n_elems * args.steps / (elapsed_ms * 1e-3)
+
+    # ---- e2e through the public API with HOST buffers (pinned), H2D + D2H inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        coords_h = coords.cpu().pin_memory()
+        coeff_h = coeff.cpu().pin_memory() if coeff is not None else None
+        vals_h = [torch.empty(plan.nnz, dtype=torch.float64, pin_memory=True) if vals[i] is not None else None
+                  for i in range(3)]
+        ke = max(1, min(args.steps, args.e2e_steps))
+        lfem.lfem_assemble_numeric_host(plan, kmask, coords_h, coeff_h, vals_h)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in range(ke):
+            lfem.lfem_assemble_numeric_host(plan, kmask, coords_h, coeff_h, vals_h)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        h2d = (n_nodes * 24 + (n_nodes * 8 if coeff is not None else 0)) * world
+        e2e = {"value": n_elems * ke / (float(te) * 1e-3), "unit": "elements/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(nnz_total * 8 * len(kinds)),
+               "api": "lfem_assemble_numeric_host", "steps": ke}
+        # e2e must produce the same bits as the device path
+        for i in range(3):
+            if vals[i] is not None:
+                assert torch.equal(vals_h[i], vals[i].cpu()), "e2e values differ from the device path"
+        del vals_h, coords_h, coeff_h
+
+    # ---- multi-GPU verification: NCCL all_gather of x + local SpMV; checksums all-reduced
+    verify = None
+    if args.verify or world > 1:
+        x = coords[:, 0].contiguous()
+        shard = (n_nodes + world - 1) // world
+        xs = torch.zeros(shard * world, dtype=torch.float64, device=dev)
+        mine = x[rank * shard:min(n_nodes, (rank + 1) * shard)]
+        loc = torch.zeros(shard, dtype=torch.float64, device=dev)
+        loc[:mine.numel()] = mine
+        if world > 1:
+            dist.all_gather_into_tensor(xs, loc)
+        else:
+            xs = loc
+        xg = xs[:n_nodes]
+        y = torch.empty(plan.n_rows, dtype=torch.float64, device=dev)
+        one = torch.ones(n_nodes, dtype=torch.float64, device=dev)
+        sums = torch.zeros(3, dtype=torch.float64, device=dev)
+        lfem.lfem_spmv(plan, vals[0], one, y)
+        sums[0] = y.sum()
+        k2 = vals[1] if vals[1] is not None else vals[2]
+        tr = 0.0
+        for c in range(3):
+            xc = coords[:, c].contiguous()
+            lfem.lfem_spmv(plan, k2, xc, y)
+            tr = tr + torch.dot(xc[r0:r1], y)
+        sums[1] = tr
+        lfem.lfem_spmv(plan, k2, xg, y)
+        sums[2] = torch.dot(xg[r0:r1], y)
+        if world > 1:
+            dist.all_reduce(sums)
+        verify = {"one_M_one": float(sums[0]), "trace_xAx": float(sums[1]), "xAx_gathered": float(sums[2]),
+                  "allgather_bytes": int(shard * world * 8)}
+
+    # ---- roofline of the numeric step
+    hbm, peak_src = peaks()
+    kern = sorted(prof.items(), key=lambda kv: -kv[1][0])
+    dom_name, (dom_ms, dom_n) = kern[0] if kern else ("numeric", (ms_per_step * nprof, nprof))
+    step_kernel_ms = sum(v[0] for v in prof.values()) / max(1, nprof)
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        traffic = tj.get(f"{name}:{dom_name}")
+    achieved = alg_bytes_rank / (step_kernel_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic,
+                "kernel": "+".join(k for k, _ in kern) if len(kern) > 1 else dom_name,
+                "algorithmic_bytes_per_launch": int(alg_bytes_rank), "kernel_ms": step_kernel_ms,
+                "peak_source": peak_src,
+                "per_kernel_ms": {k: v[0] / max(1, v[1]) for k, v in prof.items()},
+                "frac_of_8TBs_spec": alg_bytes_rank / (step_kernel_ms * 1e-3) / 8e12}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        mh = m
+        rate, rows, dt, nt, _ = oracle_sample(mh, kinds, mh.coeff if has_coeff else None, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "elements/s", "cores": nt, "kind": "oracle",
+               "sample": f"rows [0, {rows}) of {n_nodes} ({dt:.1f} s); elements/s = n_elems * rows/n_rows / t"}
+
+    if rank == 0:
+        line = {
+            "metric": "elements/s (fp64 numeric assembly of all kinds of the config into CSR)",
+            "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
+            "config": {"workload": f"{name}: {CONFIG_DESC[name]}", "kinds": list(kinds), "n_elems": n_elems,
+                       "n_nodes": n_nodes, "nnz": nnz_total, "parallelism": f"row-blocks x{world}",
+                       "l2": "flushed (256 MiB write) between steps" if flush else
+                             "inputs+outputs > L2 (126 MB); no flush", "variant": args.variant},
+            "nnz_per_s": nnz_total * args.steps / (elapsed_ms * 1e-3),
+            "value_slots_per_s": len(kinds) * nnz_total * args.steps / (elapsed_ms * 1e-3),
+            "symbolic_ms": symbolic_ms, "generate_s": gen_s,
+            "halo_factor": elems_local_total / n_elems,
+            "gpu_launches": (lfem.lfem_numeric_launches(plan, kmask) + (1 if u_work is not None else 0)) * args.steps,
+            "roofline": roofline,
+            "fp64": {"flop_model_per_elem": FLOP_PER_ELEM[name],
+                     "achieved_tflops": FLOP_PER_ELEM[name] * plan.n_elems_local / (step_kernel_ms * 1e-3) / 1e12},
+            "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "verify": verify,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--impl", default="lfem", choices=["lfem", "reference"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "v0", "tiled"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--verify", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_lfem(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -408,8 +408,11 @@ int oracle_assemble_rows(int domain, int order, int quad, int64_t n_nodes, const
         for (int64_t e = 0; e < n_elems; ++e)
             for (int a = 0; a < n; ++a) inc[cur[conn[e * n + a]]++] = e;
     }
-    // row blocks: <= BLOCK rows each
-    const int64_t BLOCK = 1 << 18;
+    // row blocks (each owned by one thread; results do not depend on the split)
+    if (nthreads < 1) nthreads = 1;
+    int64_t BLOCK = (n_rows + 4 * nthreads - 1) / (4 * (int64_t)nthreads);
+    if (BLOCK < 1024) BLOCK = 1024;
+    if (BLOCK > (1 << 18)) BLOCK = 1 << 18;
     const int64_t nblocks = (n_rows + BLOCK - 1) / BLOCK;
     std::vector<Csr> parts(nblocks);
     std::vector<int64_t> bad(nblocks, -1);
@@ -465,7 +468,6 @@ int oracle_assemble_rows(int domain, int order, int quad, int64_t n_nodes, const
         }
         for (int64_t rr = r + 1; rr <= P.n_rows; ++rr) P.row_ptr[rr] = idx;
     };
-    if (nthreads < 1) nthreads = 1;
     {
         std::vector<std::thread> pool;
         std::vector<int64_t> next(1, 0);

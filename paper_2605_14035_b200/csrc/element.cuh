@@ -1,0 +1,271 @@
+// Per-element fp64 geometry + local matrices (symmetric halves) for the
+// numeric kernels.  Included by numeric.cu after reference.cuh.
+//
+// Mathematics (§3.2, Listing 1):
+//   J(xi) = DF(xi) = sum_{j>=2} (x_j - x_1) grad_ref phi_j(xi)^T   (Eq. jacobian_inv P:317-327;
+//           differences, reading G24).  grad_ref phi_j is affine in xi for
+//           P2 (constant for P1), so J(xi) = J0 + sum_n xi_n J1_n with
+//           J0 = sum_j d_j grad phi_j(0), J1_n = sum_j d_j d_n grad phi_j: the
+//           per-element part is formed once, each quadrature point costs
+//           3*D*D FMAs (instead of 3*D*(nref-1)).
+//   surface: G = J^T J, mu = sqrt(det G), K = w mu G^{-1} = (w / mu) adj(G)
+//            A_loc(a,b) = sum_q grad_a(q)^T K_q grad_b(q)   (metric form of
+//            Eq. Aloc-precise, = Listing 1's B^T B with B = C^T grad, G2)
+//   bulk:    mu = |det J|, g_a = J^{-T} grad_a = cof(J) grad_a / det J,
+//            A_loc(a,b) = sum_q (w_q / mu_q) (cof grad_a) . (cof grad_b)
+//   M_loc(a,b)  = sum_q w_q mu_q phi_a phi_b                    (Eq. P:346)
+//   Aa_loc(a,b) = sum_q a(u_h(xi_q)) * (stiffness integrand),  a(u) = 1 + u^2
+// Evaluation order ("scalars first"): the quadrature loop produces a few
+// scalars per point (w mu, K, a); the nsym entries are then contractions of
+// those scalars with the constant tables pp / gg -- few live registers, no
+// accumulator arrays.  Bulk stiffness keeps per-entry accumulators (the
+// gradient form is cheaper than the 6-entry metric form for tets).
+#pragma once
+#include "lfem_internal.cuh"
+#include "reference.cuh"
+
+// Coefficients of the reference shape-function derivatives (small integers):
+//   d phi_j / d xi_m (xi) = SA(j,m) + sum_n SB(j,m,n) xi_n
+template <int D, int ORDER>
+struct Shape {
+    static constexpr int NV = D + 1;
+    static constexpr int N = ORDER == 1 ? NV : NV + (D == 2 ? 3 : 6);
+    __host__ __device__ static constexpr int g(int k, int m) { return k == 0 ? -1 : (k == m + 1 ? 1 : 0); }
+    __host__ __device__ static constexpr int c(int k) { return k == 0 ? 1 : 0; }
+    __host__ __device__ static constexpr int ei(int e) {
+        return D == 2 ? (e == 0 ? 0 : e == 1 ? 1 : 2) : (e == 0 ? 0 : e == 1 ? 1 : e == 2 ? 2 : e == 3 ? 0 : e == 4 ? 1 : 2);
+    }
+    __host__ __device__ static constexpr int ej(int e) {
+        return D == 2 ? (e == 0 ? 1 : e == 1 ? 2 : 0) : (e == 0 ? 1 : e == 1 ? 2 : e == 2 ? 0 : 3);
+    }
+    __host__ __device__ static constexpr int SA(int j, int m) {
+        if (ORDER == 1) return g(j, m);
+        if (j < NV) return (4 * c(j) - 1) * g(j, m);
+        const int e = j - NV, i = ei(e), k = ej(e);
+        return 4 * (c(i) * g(k, m) + c(k) * g(i, m));
+    }
+    __host__ __device__ static constexpr int SB(int j, int m, int n) {
+        if (ORDER == 1) return 0;
+        if (j < NV) return 4 * g(j, n) * g(j, m);
+        const int e = j - NV, i = ei(e), k = ej(e);
+        return 4 * (g(i, n) * g(k, m) + g(k, n) * g(i, m));
+    }
+};
+
+template <int F> struct FamShape;
+template <> struct FamShape<FAM_TRI_P1> { using S = Shape<2, 1>; };
+template <> struct FamShape<FAM_TRI_P2> { using S = Shape<2, 2>; };
+template <> struct FamShape<FAM_TET_P1> { using S = Shape<3, 1>; };
+template <> struct FamShape<FAM_TET_P2> { using S = Shape<3, 2>; };
+
+// Branch-free fp64 reciprocal square root / reciprocal: hardware approximation
+// (MUFU.RSQ64H / MUFU.RCP64H) + two Newton steps (error ~1 ulp).  CUDA's
+// rsqrt()/division carry a slow-path branch per call, which splits the
+// unrolled quadrature loop into scheduling regions.  Non-positive or
+// non-finite arguments are flagged as degenerate by the caller.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double e = fma(-x * r, r, 1.0);  // 1 - x r^2
+        r = fma(0.5 * r, e, r);
+    }
+    return r;
+}
+
+__device__ __forceinline__ double rcp_nr(double x) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double e = fma(-x, r, 1.0);
+        r = fma(r, e, r);
+    }
+    return r;
+}
+
+// reference coordinates of the quadrature points (constant memory)
+struct QuadXi {
+    double xi[11][3];
+};
+__constant__ QuadXi c_xi[4];
+
+template <int F, bool DM, bool DA, bool DAA>
+struct Element {
+    static constexpr int N = FamInfo<F>::NREF, D = FamInfo<F>::D, NQ = FamInfo<F>::NQ, NS = FamInfo<F>::NSYM;
+    using S = typename FamShape<F>::S;
+    static_assert(S::N == N, "shape table");
+
+    // J0[c][m], J1[c][m][n] (n >= m used; symmetric) from differences d_j = x_j - x_1
+    static __device__ __forceinline__ void jac_parts(const double (&X)[N][3], double (&J0)[3][D],
+                                                     double (&J1)[3][D][D]) {
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+            double d[N];
+#pragma unroll
+            for (int j = 1; j < N; ++j) d[j] = X[j][cc] - X[0][cc];
+#pragma unroll
+            for (int m = 0; m < D; ++m) {
+                double s = 0.0;
+#pragma unroll
+                for (int j = 1; j < N; ++j)
+                    if (S::SA(j, m) != 0) s = fma((double)S::SA(j, m), d[j], s);
+                J0[cc][m] = s;
+#pragma unroll
+                for (int n = 0; n < D; ++n) {
+                    double t = 0.0;
+#pragma unroll
+                    for (int j = 1; j < N; ++j)
+                        if (S::SB(j, m, n) != 0) t = fma((double)S::SB(j, m, n), d[j], t);
+                    J1[cc][m][n] = t;
+                }
+            }
+        }
+    }
+
+    static __device__ __forceinline__ void jac_at(const double (&J0)[3][D], const double (&J1)[3][D][D], int q,
+                                                  double (&J)[3][D]) {
+        constexpr int FI = F;
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+            for (int m = 0; m < D; ++m) {
+                double v = J0[cc][m];
+                if (N > D + 1) {  // P2: affine in xi
+#pragma unroll
+                    for (int n = 0; n < D; ++n) v = fma(c_xi[FI].xi[q][n], J1[cc][m][n], v);
+                }
+                J[cc][m] = v;
+            }
+    }
+
+    // Computes all requested symmetric local entries and hands each to
+    // sink(kind 0/1/2, s, value) exactly once.  Returns false if mu <= 0 or
+    // non-finite at some quadrature point.
+    template <class Sink>
+    static __device__ __forceinline__ bool compute(const double (&X)[N][3], const double (&U)[N], Sink& sink) {
+        const RefTab<F>& T = tab<F>();
+        double J0[3][D], J1[3][D][D];
+        jac_parts(X, J0, J1);
+        bool ok = true;
+        if (D == 2) {
+            double wmu[NQ], k11[NQ], k12[NQ], k22[NQ], aq[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                double J[3][D];
+                jac_at(J0, J1, q, J);
+                const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+                const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
+                const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
+                const double det = g11 * g22 - g12 * g12;
+                ok &= (det > 0.0) & (det < INFINITY);
+                const double r = rsqrt_nr(det);
+                wmu[q] = T.w[q] * (det * r);
+                const double c = T.w[q] * r;
+                k11[q] = c * g22;
+                k12[q] = -c * g12;
+                k22[q] = c * g11;
+                if (DAA) {
+                    double u = 0.0;
+#pragma unroll
+                    for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
+                    aq[q] = fma(u, u, 1.0);
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (DM) {
+                    double m = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) m = fma(wmu[q], T.pp[q][s], m);
+                    sink(0, s, m);
+                }
+                if (DA || DAA) {
+                    double a = 0.0, aa = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        double st = k11[q] * T.gg[q][s][0];
+                        st = fma(k12[q], T.gg[q][s][1], st);
+                        st = fma(k22[q], T.gg[q][s][2], st);
+                        if (DA) a += st;
+                        if (DAA) aa = fma(aq[q], st, aa);
+                    }
+                    if (DA) sink(1, s, a);
+                    if (DAA) sink(2, s, aa);
+                }
+            }
+        } else {
+            double wmu[NQ];
+            double A[(DA ? NS : 1)], Aa[(DAA ? NS : 1)];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (DA) A[s] = 0.0;
+                if (DAA) Aa[s] = 0.0;
+            }
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                double J[3][D];
+                jac_at(J0, J1, q, J);
+                double C[3][3];
+                C[0][0] = J[1][1 % D] * J[2][2 % D] - J[1][2 % D] * J[2][1 % D];
+                C[0][1] = J[1][2 % D] * J[2][0] - J[1][0] * J[2][2 % D];
+                C[0][2] = J[1][0] * J[2][1 % D] - J[1][1 % D] * J[2][0];
+                C[1][0] = J[0][2 % D] * J[2][1 % D] - J[0][1 % D] * J[2][2 % D];
+                C[1][1] = J[0][0] * J[2][2 % D] - J[0][2 % D] * J[2][0];
+                C[1][2] = J[0][1 % D] * J[2][0] - J[0][0] * J[2][1 % D];
+                C[2][0] = J[0][1 % D] * J[1][2 % D] - J[0][2 % D] * J[1][1 % D];
+                C[2][1] = J[0][2 % D] * J[1][0] - J[0][0] * J[1][2 % D];
+                C[2][2] = J[0][0] * J[1][1 % D] - J[0][1 % D] * J[1][0];
+                const double det = J[0][0] * C[0][0] + J[0][1 % D] * C[0][1] + J[0][2 % D] * C[0][2];
+                const double adet = fabs(det);
+                ok &= (adet > 0.0) & (adet < INFINITY);
+                wmu[q] = T.w[q] * adet;
+                if (DA || DAA) {
+                    const double c = T.w[q] * rcp_nr(adet);
+                    double aq = 1.0;
+                    if (DAA) {
+                        double u = 0.0;
+#pragma unroll
+                        for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
+                        aq = fma(u, u, 1.0);
+                    }
+                    double g[N][3], h[N][3];
+#pragma unroll
+                    for (int a = 0; a < N; ++a)
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            double acc = C[k][0] * T.dphi[q][a][0];
+                            acc = fma(C[k][1], T.dphi[q][a][1 % D], acc);
+                            acc = fma(C[k][2], T.dphi[q][a][2 % D], acc);
+                            g[a][k] = acc;
+                            h[a][k] = c * acc;
+                        }
+#pragma unroll
+                    for (int a = 0; a < N; ++a)
+#pragma unroll
+                        for (int b = a; b < N; ++b) {
+                            const int s = sym_index(N, a, b);
+                            double st = h[a][0] * g[b][0];
+                            st = fma(h[a][1], g[b][1], st);
+                            st = fma(h[a][2], g[b][2], st);
+                            if (DA) A[s] += st;
+                            if (DAA) Aa[s] = fma(aq, st, Aa[s]);
+                        }
+                }
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) {
+                if (DM) {
+                    double m = 0.0;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) m = fma(wmu[q], T.pp[q][s], m);
+                    sink(0, s, m);
+                }
+                if (DA) sink(1, s, A[s]);
+                if (DAA) sink(2, s, Aa[s]);
+            }
+        }
+        return ok;
+    }
+};

@@ -1,0 +1,128 @@
+// Internal definitions of liblfem (B200, sm_100a).  Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/lfem.h"
+
+// ---------------------------------------------------------------------------
+// element families
+// ---------------------------------------------------------------------------
+enum Family { FAM_TRI_P1 = 0, FAM_TRI_P2 = 1, FAM_TET_P1 = 2, FAM_TET_P2 = 3 };
+
+template <int F> struct FamInfo;
+template <> struct FamInfo<FAM_TRI_P1> { static constexpr int NREF = 3, D = 2, NQ = 3, NSYM = 6; };
+template <> struct FamInfo<FAM_TRI_P2> { static constexpr int NREF = 6, D = 2, NQ = 6, NSYM = 21; };
+template <> struct FamInfo<FAM_TET_P1> { static constexpr int NREF = 4, D = 3, NQ = 4, NSYM = 10; };
+template <> struct FamInfo<FAM_TET_P2> { static constexpr int NREF = 10, D = 3, NQ = 11, NSYM = 55; };
+
+// index of (a, b), a <= b, in the row-major upper triangle of an n x n matrix
+__host__ __device__ constexpr int sym_index(int n, int a, int b) {
+    return a <= b ? a * n - a * (a - 1) / 2 + (b - a) : b * n - b * (b - 1) / 2 + (a - b);
+}
+
+// ---------------------------------------------------------------------------
+// handles
+// ---------------------------------------------------------------------------
+struct lfem_mesh_s {
+    int domain, order, quad, family, nref, nq, nsym;
+    int64_t n_nodes, n_elems;
+    const double* coords;
+    const int32_t* conn;
+};
+
+// Row-tile plan of the fused numeric kernel.
+struct TilePlan {
+    int n_tiles = 0;
+    int rows_per_tile = 0;
+    int max_tile_elems = 0;     // max elements per tile (smem sizing)
+    int max_tile_slots = 0;
+    int max_tile_codes = 0;
+    int built_nk = 0;                   // kinds count the tile size was chosen for
+    int32_t* tile_elem_ptr = nullptr;   // n_tiles + 1 (into tile_elems)
+    int32_t* tile_elems = nullptr;      // plan-local element ids, ascending per tile
+    int32_t* tile_conn_ptr = nullptr;   // n_tiles + 1 (int32 offsets into tile_conn, multiples of 4)
+    int32_t* tile_conn = nullptr;       // per tile: its elements' connectivity in tile order
+    int4* tile_info = nullptr;          // 2 per tile: {s0, ns, c0, nc}, {e0, ne, q0, nq}
+    int32_t* tile_code_ptr = nullptr;   // n_tiles + 1 (into codes16)
+    uint16_t* codes16 = nullptr;        // per slot, per contribution: elem_in_tile*NSYM + sym
+    uint8_t* slot_cnt = nullptr;        // nnz: contributions per slot
+    size_t smem_bytes = 0;
+    bool ready = false;
+};
+
+struct Profiler;  // api.cu
+void prof_begin(lfem_plan_s* p, const char* name, cudaStream_t s);
+void prof_end(lfem_plan_s* p, cudaStream_t s);
+
+struct lfem_plan_s {
+    lfem_mesh_s* mesh = nullptr;
+    int64_t row_begin = 0, row_end = 0, n_rows = 0, nnz = 0, n_local = 0, n_contrib = 0;
+    int32_t* elem_list = nullptr;   // n_local: global element ids, ascending
+    int32_t* local_conn = nullptr;  // n_local x nref copy of the connectivity (plan order)
+    int64_t* row_ptr = nullptr;     // n_rows + 1
+    int32_t* col_idx = nullptr;     // nnz (global)
+    int32_t* slot_ptr = nullptr;    // nnz + 1 into codes
+    int32_t* codes = nullptr;       // n_contrib: sym * n_local + local element
+    double* stage = nullptr;        // v0 staging: 3 x nsym x n_local
+    int* err = nullptr;             // device: lowest degenerate element id (INT_MAX = none)
+    int variant = LFEM_NUMERIC_AUTO;
+    TilePlan tiles;
+    Profiler* prof = nullptr;
+    // e2e staging (lfem_assemble_numeric_host)
+    double* d_coords = nullptr;
+    double* d_coeff = nullptr;
+    double* d_vals[3] = {nullptr, nullptr, nullptr};
+};
+
+// ---------------------------------------------------------------------------
+// error state (thread-local, set by every failing entry point)
+// ---------------------------------------------------------------------------
+lfem_status lfem_fail(lfem_status st, const std::string& msg, int64_t elem = -1);
+lfem_status lfem_cuda_fail(cudaError_t e, const char* what);
+
+#define LFEM_CUDA(call)                                            \
+    do {                                                           \
+        cudaError_t e_ = (call);                                   \
+        if (e_ != cudaSuccess) return lfem_cuda_fail(e_, #call);   \
+    } while (0)
+
+#define LFEM_TRY(call)                                             \
+    do {                                                           \
+        lfem_status s_ = (call);                                   \
+        if (s_ != LFEM_OK) return s_;                              \
+    } while (0)
+
+// device memory helpers (cudaMallocAsync on the plan's stream)
+lfem_status dev_alloc(void** p, size_t bytes, cudaStream_t s);
+void dev_free(void* p, cudaStream_t s);
+template <class T>
+inline lfem_status dev_alloc_t(T** p, size_t n, cudaStream_t s) {
+    return dev_alloc(reinterpret_cast<void**>(p), n * sizeof(T) + 16, s);
+}
+
+// scan.cu: out[0] = 0, out[i+1] = sum_{j<=i} in[j]  (n+1 outputs)
+lfem_status scan_exclusive_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);
+
+// symbolic.cu
+lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s);
+lfem_status build_tiles(lfem_plan_s* p, int rows_per_tile, cudaStream_t s);
+void free_tiles(TilePlan& t, cudaStream_t s);
+
+// numeric.cu
+lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
+                             double* const vals[3], cudaStream_t s);
+int numeric_launch_count(lfem_plan_s* p, unsigned kinds);
+lfem_status spmv_launch(lfem_plan_s* p, const double* vals, const double* x, double* y, cudaStream_t s);
+lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const double* b, double* out,
+                         cudaStream_t s);
+lfem_status upload_reference_tables();
+lfem_status check_conn_launch(const int32_t* conn, int64_t n_elems, int nref, int64_t n_nodes, int* bad,
+                              cudaStream_t s);
+
+inline int family_of(int domain, int order) {
+    if (domain == LFEM_SURFACE_TRI) return order == 1 ? FAM_TRI_P1 : FAM_TRI_P2;
+    return order == 1 ? FAM_TET_P1 : FAM_TET_P2;
+}

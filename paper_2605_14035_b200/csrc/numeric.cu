@@ -1,0 +1,243 @@
+// Numeric phase of the ℓFEM assembly on B200 (sm_100a), fp64.
+//
+// Per element (Listing 1 P:581-609 and §3.2):
+//   gather the nref node coordinates (Listing 1 l.12),
+//   J(xi_q) = sum_{j>=2} (x_j - x_1) grad_ref phi_j(xi_q)^T  (Eq. jacobian_inv P:317-327,
+//             differences: reading G24),
+//   surface: G = J^T J, mu = sqrt(det G) (= |t1 x t2|, Listing 1 l.16-17),
+//            K_q = w_q mu G^{-1} (metric form of Eq. Aloc-precise P:337 with C = L^{-1}
+//            read as Listing 1, reading G2), A_loc(a,b) += grad_a^T K_q grad_b;
+//   bulk:    mu = |det J|, g_a = J^{-T} grad_a = cof(J) grad_a / det J,
+//            A_loc(a,b) += (w_q / mu) (cof grad_a).(cof grad_b);
+//   M_loc(a,b) += w_q mu phi_a phi_b                      (Eq. reference_quadrature_mass),
+//   A_a,loc(a,b) += a(u_h(xi_q)) * (stiffness integrand),
+//            u_h(xi_q) = sum_c u_c phi_c(xi_q), a(u) = 1 + u^2 (north_star, reading G10).
+// Only the symmetric half (a <= b) is computed.  Reduction into CSR follows
+// the plan built by symbolic.cu: every slot sums its contributions in
+// ascending (element, a, b) order (reading G21) -- no atomics.
+//
+// Variants:
+//   V0     k_elem_v0 (thread per element -> staged local matrices in HBM)
+//          + k_slot_reduce (thread per CSR slot).
+//   TILED  see numeric_tiled.cuh.
+#include <climits>
+#include <mutex>
+
+#include "lfem_internal.cuh"
+#include "reference.cuh"
+#include "element.cuh"
+
+namespace {
+
+// --------------------------------------------------------------------------
+// V0: element kernel -> stage[k][s][le]; slot kernel -> vals
+// --------------------------------------------------------------------------
+struct GlobalStageSink {
+    double* stage;
+    int64_t n_local, le;
+    __device__ __forceinline__ void operator()(int k, int s, double v) const {
+        stage[(int64_t)k * nsym_stride + (int64_t)s * n_local + le] = v;
+    }
+    int64_t nsym_stride;
+};
+
+template <int F, bool DM, bool DA, bool DAA>
+__global__ void __launch_bounds__(128)
+k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __restrict__ elem_list,
+          const double* __restrict__ coords, const double* __restrict__ coeff, double* __restrict__ stage,
+          int* __restrict__ err) {
+    using E = Element<F, DM, DA, DAA>;
+    constexpr int N = E::N, NS = E::NS;
+    for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < n_local;
+         le += (int64_t)gridDim.x * blockDim.x) {
+        double X[N][3], U[N];
+#pragma unroll
+        for (int a = 0; a < N; ++a) {
+            const int64_t v = __ldg(&lconn[le * N + a]);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) X[a][c] = __ldg(&coords[3 * v + c]);
+            U[a] = DAA ? __ldg(&coeff[v]) : 0.0;
+        }
+        GlobalStageSink sink{stage, n_local, le, (int64_t)NS * n_local};
+        if (!E::compute(X, U, sink)) atomicMin(err, __ldg(&elem_list[le]));
+    }
+}
+
+template <bool DM, bool DA, bool DAA>
+__global__ void __launch_bounds__(256)
+k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ codes,
+              const double* __restrict__ stage, int64_t stride, double* __restrict__ vm, double* __restrict__ va,
+              double* __restrict__ vaa) {
+    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * blockDim.x) {
+        const int j0 = __ldg(&slot_ptr[s]), j1 = __ldg(&slot_ptr[s + 1]);
+        double m = 0.0, a = 0.0, aa = 0.0;
+        for (int j = j0; j < j1; ++j) {
+            const int64_t c = __ldg(&codes[j]);
+            if (DM) m += __ldg(&stage[c]);
+            if (DA) a += __ldg(&stage[stride + c]);
+            if (DAA) aa += __ldg(&stage[2 * stride + c]);
+        }
+        if (DM) vm[s] = m;
+        if (DA) va[s] = a;
+        if (DAA) vaa[s] = aa;
+    }
+}
+
+inline unsigned grid_for(int64_t n, int threads, int max_blocks) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > max_blocks) g = max_blocks;
+    return (unsigned)g;
+}
+
+template <int F, bool DM, bool DA, bool DAA>
+lfem_status run_v0(lfem_plan_s* p, const double* coords, const double* coeff, double* const vals[3], cudaStream_t s) {
+    constexpr int NS = FamInfo<F>::NSYM;
+    if (!p->stage) LFEM_TRY(dev_alloc_t(&p->stage, (size_t)3 * NS * p->n_local + 1, s));
+    if (p->n_local > 0) {
+        prof_begin(p, "k_elem_v0", s);
+        k_elem_v0<F, DM, DA, DAA><<<grid_for(p->n_local, 128, 1 << 20), 128, 0, s>>>(
+            p->n_local, p->local_conn, p->elem_list, coords, coeff, p->stage, p->err);
+        LFEM_CUDA(cudaGetLastError());
+        prof_end(p, s);
+    }
+    if (p->nnz > 0) {
+        prof_begin(p, "k_slot_reduce", s);
+        k_slot_reduce<DM, DA, DAA><<<grid_for(p->nnz, 256, 1 << 20), 256, 0, s>>>(
+            p->nnz, p->slot_ptr, p->codes, p->stage, (int64_t)NS * p->n_local, vals[0], vals[1], vals[2]);
+        LFEM_CUDA(cudaGetLastError());
+        prof_end(p, s);
+    }
+    return LFEM_OK;
+}
+
+template <int F>
+lfem_status dispatch_kinds(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
+                           double* const vals[3], cudaStream_t s) {
+    switch (kinds) {
+    case 1: return run_v0<F, true, false, false>(p, coords, coeff, vals, s);
+    case 2: return run_v0<F, false, true, false>(p, coords, coeff, vals, s);
+    case 3: return run_v0<F, true, true, false>(p, coords, coeff, vals, s);
+    case 4: return run_v0<F, false, false, true>(p, coords, coeff, vals, s);
+    case 5: return run_v0<F, true, false, true>(p, coords, coeff, vals, s);
+    case 6: return run_v0<F, false, true, true>(p, coords, coeff, vals, s);
+    case 7: return run_v0<F, true, true, true>(p, coords, coeff, vals, s);
+    default: return lfem_fail(LFEM_ERR_INVALID_ARG, "kinds must be a nonzero subset of MASS|STIFF|STIFF_COEF");
+    }
+}
+
+// --------------------------------------------------------------------------
+// misc kernels
+// --------------------------------------------------------------------------
+__global__ void k_check_conn(const int32_t* __restrict__ conn, int64_t n_elems, int nref, int64_t n_nodes,
+                             int* __restrict__ bad) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_elems;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        bool ok = true;
+        for (int a = 0; a < nref; ++a) {
+            const int64_t v = conn[e * nref + a];
+            ok &= (v >= 0) & (v < n_nodes);
+        }
+        if (!ok) atomicMin(bad, (int)e);
+    }
+}
+
+__global__ void k_spmv(int64_t n_rows, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                       const double* __restrict__ vals, const double* __restrict__ x, double* __restrict__ y) {
+    // one warp per row; lanes stride the row, fixed-order tree reduction
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w; r < n_rows; r += nw) {
+        double acc = 0.0;
+        for (int64_t j = row_ptr[r] + lane; j < row_ptr[r + 1]; j += 32) acc = fma(vals[j], x[col[j]], acc);
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) y[r] = acc;
+    }
+}
+
+__global__ void k_axpby(int64_t n, double ca, const double* __restrict__ a, double cb, const double* __restrict__ b,
+                        double* __restrict__ out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = ca * a[i] + cb * b[i];
+}
+
+std::mutex g_tab_mu;
+uint64_t g_tab_devices = 0;  // bit per device with uploaded tables
+
+}  // namespace
+
+#include "numeric_tiled.cuh"
+
+lfem_status upload_reference_tables() {
+    int dev = 0;
+    LFEM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_tab_mu);
+    if (dev < 64 && (g_tab_devices >> dev) & 1ull) return LFEM_OK;
+    static RefTab<FAM_TRI_P1> t1;
+    static RefTab<FAM_TRI_P2> t2;
+    static RefTab<FAM_TET_P1> t3;
+    static RefTab<FAM_TET_P2> t4;
+    refhost::fill(t1, refhost::rule_tri3(), 2, 1);
+    refhost::fill(t2, refhost::rule_tri6(), 2, 2);
+    refhost::fill(t3, refhost::rule_tet4(), 3, 1);
+    refhost::fill(t4, refhost::rule_tet11(), 3, 2);
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri1, &t1, sizeof(t1)));
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri2, &t2, sizeof(t2)));
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tet1, &t3, sizeof(t3)));
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tet2, &t4, sizeof(t4)));
+    QuadXi xi[4] = {};
+    const refhost::Rule rules[4] = {refhost::rule_tri3(), refhost::rule_tri6(), refhost::rule_tet4(),
+                                    refhost::rule_tet11()};
+    for (int f = 0; f < 4; ++f)
+        for (int q = 0; q < rules[f].nq; ++q)
+            for (int m = 0; m < 3; ++m) xi[f].xi[q][m] = rules[f].xi[q][m];
+    LFEM_CUDA(cudaMemcpyToSymbol(c_xi, xi, sizeof(xi)));
+    if (dev < 64) g_tab_devices |= (1ull << dev);
+    return LFEM_OK;
+}
+
+lfem_status check_conn_launch(const int32_t* conn, int64_t n_elems, int nref, int64_t n_nodes, int* bad,
+                              cudaStream_t s) {
+    if (n_elems == 0) return LFEM_OK;
+    k_check_conn<<<grid_for(n_elems, 256, 148 * 32), 256, 0, s>>>(conn, n_elems, nref, n_nodes, bad);
+    LFEM_CUDA(cudaGetLastError());
+    return LFEM_OK;
+}
+
+lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
+                             double* const vals[3], cudaStream_t s) {
+    LFEM_TRY(upload_reference_tables());
+    const int fam = p->mesh->family;
+    const int variant = p->variant == LFEM_NUMERIC_AUTO ? tiled_default_variant(p) : p->variant;
+    if (variant == LFEM_NUMERIC_TILED) return tiled_dispatch(p, kinds, coords, coeff, vals, s);
+    switch (fam) {
+    case FAM_TRI_P1: return dispatch_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
+    case FAM_TRI_P2: return dispatch_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);
+    case FAM_TET_P1: return dispatch_kinds<FAM_TET_P1>(p, kinds, coords, coeff, vals, s);
+    case FAM_TET_P2: return dispatch_kinds<FAM_TET_P2>(p, kinds, coords, coeff, vals, s);
+    }
+    return lfem_fail(LFEM_ERR_UNSUPPORTED, "family");
+}
+
+int numeric_launch_count(lfem_plan_s* p, unsigned kinds) {
+    (void)kinds;
+    const int variant = p->variant == LFEM_NUMERIC_AUTO ? tiled_default_variant(p) : p->variant;
+    if (variant == LFEM_NUMERIC_TILED) return tiled_launch_count(p);
+    return (p->n_local > 0 ? 1 : 0) + (p->nnz > 0 ? 1 : 0);
+}
+
+lfem_status spmv_launch(lfem_plan_s* p, const double* vals, const double* x, double* y, cudaStream_t s) {
+    if (p->n_rows == 0) return LFEM_OK;
+    k_spmv<<<grid_for(p->n_rows * 32, 256, 148 * 64), 256, 0, s>>>(p->n_rows, p->row_ptr, p->col_idx, vals, x, y);
+    LFEM_CUDA(cudaGetLastError());
+    return LFEM_OK;
+}
+
+lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const double* b, double* out,
+                         cudaStream_t s) {
+    if (n == 0) return LFEM_OK;
+    k_axpby<<<grid_for(n, 256, 148 * 16), 256, 0, s>>>(n, ca, a, cb, b, out);
+    LFEM_CUDA(cudaGetLastError());
+    return LFEM_OK;
+}

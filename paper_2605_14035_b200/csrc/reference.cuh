@@ -1,0 +1,161 @@
+// Reference-element tables of liblfem, in __constant__ memory -- the B200
+// counterpart of ℓFEM's precompute_surface_dD_Pk / precompute_bulk_dD_Pk
+// (§5.2; Listing 1 l.4-7 P:585-588).  Computed on the
+// host from the closed-form Lagrange basis (PAPER.md Eq. form_functions_s2dp2
+// P:268-273 with the Lagrange vertex functions of reading G1; tet edge order
+// G26) and the quadrature rules fixed by BASELINE.json (readings G6-G9).
+//
+// Include in exactly ONE translation unit (numeric.cu): __constant__ symbols
+// are per-TU without relocatable device code.
+//
+// Per quadrature point q (symmetric half index s = sym(a,b), a <= b):
+//   w[q], phi[q][a], dphi[q][a][m]            basis values / reference gradients
+//   pp[q][s]     = phi_a phi_b                  (mass integrand, Eq. reference_quadrature_mass)
+//   gg[q][s][0..2] = d1a d1b, d1a d2b + d2a d1b, d2a d2b
+//                  (surface metric form of Eq. Aloc-precise P:337:
+//                   grad_a . C C^T grad_b = d_a^T G^{-1} d_b)
+#pragma once
+#include <cmath>
+
+#include "lfem_internal.cuh"
+
+template <int F>
+struct RefTab {
+    static constexpr int NREF = FamInfo<F>::NREF, D = FamInfo<F>::D, NQ = FamInfo<F>::NQ,
+                         NSYM = FamInfo<F>::NSYM;
+    double w[NQ];
+    double phi[NQ][NREF];
+    double dphi[NQ][NREF][D];
+    double pp[NQ][NSYM];
+    double gg[NQ][NSYM][3];
+};
+
+__constant__ RefTab<FAM_TRI_P1> c_tab_tri1;
+__constant__ RefTab<FAM_TRI_P2> c_tab_tri2;
+__constant__ RefTab<FAM_TET_P1> c_tab_tet1;
+__constant__ RefTab<FAM_TET_P2> c_tab_tet2;
+
+template <int F> __device__ __forceinline__ const RefTab<F>& tab();
+template <> __device__ __forceinline__ const RefTab<FAM_TRI_P1>& tab<FAM_TRI_P1>() { return c_tab_tri1; }
+template <> __device__ __forceinline__ const RefTab<FAM_TRI_P2>& tab<FAM_TRI_P2>() { return c_tab_tri2; }
+template <> __device__ __forceinline__ const RefTab<FAM_TET_P1>& tab<FAM_TET_P1>() { return c_tab_tet1; }
+template <> __device__ __forceinline__ const RefTab<FAM_TET_P2>& tab<FAM_TET_P2>() { return c_tab_tet2; }
+
+namespace refhost {
+
+// quadrature points in reference coordinates xi (d = 2: (xi1, xi2); d = 3)
+struct Rule {
+    int nq;
+    double xi[11][3];
+    double w[11];
+};
+
+inline Rule rule_tri3() {
+    Rule r{};
+    r.nq = 3;
+    const double t = 1.0 / 6.0, u = 2.0 / 3.0;
+    const double P[3][2] = {{t, t}, {u, t}, {t, u}};
+    for (int q = 0; q < 3; ++q) { r.xi[q][0] = P[q][0]; r.xi[q][1] = P[q][1]; r.w[q] = 1.0 / 6.0; }
+    return r;
+}
+
+inline Rule rule_tri6() {
+    Rule r{};
+    r.nq = 6;
+    const double a = 0.44594849091596488632, b = 0.09157621350977074346;
+    const double wa = 0.2233815896780114657 * 0.5, wb = 0.10995174365532186764 * 0.5;
+    const double P[6][2] = {{a, a}, {1.0 - 2.0 * a, a}, {a, 1.0 - 2.0 * a},
+                            {b, b}, {1.0 - 2.0 * b, b}, {b, 1.0 - 2.0 * b}};
+    for (int q = 0; q < 6; ++q) {
+        r.xi[q][0] = P[q][0];
+        r.xi[q][1] = P[q][1];
+        r.w[q] = q < 3 ? wa : wb;
+    }
+    return r;
+}
+
+inline Rule rule_tet4() {
+    Rule r{};
+    r.nq = 4;
+    const double al = (5.0 - std::sqrt(5.0)) / 20.0, be = (5.0 + 3.0 * std::sqrt(5.0)) / 20.0;
+    const double P[4][3] = {{al, al, al}, {be, al, al}, {al, be, al}, {al, al, be}};
+    for (int q = 0; q < 4; ++q) {
+        for (int m = 0; m < 3; ++m) r.xi[q][m] = P[q][m];
+        r.w[q] = 1.0 / 24.0;
+    }
+    return r;
+}
+
+inline Rule rule_tet11() {
+    Rule r{};
+    r.nq = 11;
+    const double c = 1.0 / 14.0, C = 11.0 / 14.0;
+    const double s = std::sqrt(5.0 / 14.0);
+    const double a = 0.25 * (1.0 + s), b = 0.25 * (1.0 - s);
+    const double P[11][3] = {{0.25, 0.25, 0.25},
+                             {c, c, c}, {C, c, c}, {c, C, c}, {c, c, C},
+                             {a, b, b}, {b, a, b}, {b, b, a}, {a, a, b}, {a, b, a}, {b, a, a}};
+    for (int q = 0; q < 11; ++q) {
+        for (int m = 0; m < 3; ++m) r.xi[q][m] = P[q][m];
+        r.w[q] = q == 0 ? -74.0 / 5625.0 : (q < 5 ? 343.0 / 45000.0 : 56.0 / 2250.0);
+    }
+    return r;
+}
+
+// Lagrange basis at xi: values and gradients w.r.t. xi.
+// barycentric l0 = 1 - sum xi, l_k = xi_k; grad l0 = (-1,..), grad l_k = e_k.
+inline void basis_eval(int d, int order, const double* xi, double* phi, double (*dphi)[3]) {
+    double l[4], gl[4][3];
+    l[0] = 1.0;
+    for (int m = 0; m < d; ++m) l[0] -= xi[m];
+    for (int m = 0; m < 3; ++m) gl[0][m] = (m < d) ? -1.0 : 0.0;
+    for (int k = 1; k <= d; ++k) {
+        l[k] = xi[k - 1];
+        for (int m = 0; m < 3; ++m) gl[k][m] = (m == k - 1) ? 1.0 : 0.0;
+    }
+    const int nv = d + 1;
+    if (order == 1) {
+        for (int a = 0; a < nv; ++a) {
+            phi[a] = l[a];
+            for (int m = 0; m < 3; ++m) dphi[a][m] = gl[a][m];
+        }
+        return;
+    }
+    for (int a = 0; a < nv; ++a) {
+        phi[a] = l[a] * (2.0 * l[a] - 1.0);
+        for (int m = 0; m < 3; ++m) dphi[a][m] = (4.0 * l[a] - 1.0) * gl[a][m];
+    }
+    static const int e2[3][2] = {{0, 1}, {1, 2}, {2, 0}};
+    static const int e3[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
+    const int ne = d == 2 ? 3 : 6;
+    for (int k = 0; k < ne; ++k) {
+        const int i = d == 2 ? e2[k][0] : e3[k][0];
+        const int j = d == 2 ? e2[k][1] : e3[k][1];
+        phi[nv + k] = 4.0 * l[i] * l[j];
+        for (int m = 0; m < 3; ++m) dphi[nv + k][m] = 4.0 * (gl[i][m] * l[j] + l[i] * gl[j][m]);
+    }
+}
+
+template <int F>
+void fill(RefTab<F>& t, const Rule& r, int d, int order) {
+    constexpr int N = RefTab<F>::NREF;
+    for (int q = 0; q < RefTab<F>::NQ; ++q) {
+        double phi[10], dphi[10][3];
+        basis_eval(d, order, r.xi[q], phi, dphi);
+        t.w[q] = r.w[q];
+        for (int a = 0; a < N; ++a) {
+            t.phi[q][a] = phi[a];
+            for (int m = 0; m < d; ++m) t.dphi[q][a][m] = dphi[a][m];
+        }
+        for (int a = 0; a < N; ++a)
+            for (int b = a; b < N; ++b) {
+                const int s = sym_index(N, a, b);
+                t.pp[q][s] = phi[a] * phi[b];
+                t.gg[q][s][0] = dphi[a][0] * dphi[b][0];
+                t.gg[q][s][1] = dphi[a][0] * dphi[b][1] + dphi[a][1] * dphi[b][0];
+                t.gg[q][s][2] = dphi[a][1] * dphi[b][1];
+            }
+    }
+}
+
+}  // namespace refhost

@@ -1,0 +1,285 @@
+// Symbolic phase of the ℓFEM assembly on B200: CSR pattern + reduction plan.
+//
+// PAPER.md §4.2: MATLAB's `sparse(I,J,V)` sorts the nE*nref^2
+// index triplets and sums duplicates on EVERY assembly ("The log-linear
+// asymptotic arises solely from sorting and summing duplicate
+// contributions"); the paper names, but does not use, the alternative of
+// "precomputing the sparsity structure ... sort-free assignment".  This file
+// is that precomputation, done once per topology on the device:
+//
+//   1. k_flag/k_compact: elements touching the owned rows [rb, re), ascending
+//      id (row-block partition with duplicated halo elements).
+//   2. k_count/k_fill/k_sort_inc: one-digit LSD radix (counting) sort of the
+//      element-local rows (e, a) by global row conn[e,a]; inside a row the
+//      incidences are then sorted by (e, a) so every later order is
+//      deterministic (reading G21).
+//   3. k_row_pattern<0>: per row (one warp), the candidate columns
+//      conn[e, b] of all incident (e, a) -- segmented sort + unique by rank
+//      counting in shared memory -> row length; exclusive scan -> row_ptr.
+//   4. k_row_pattern<1>: col_idx (ascending) and the reduction plan: for
+//      every CSR slot the list of its contributions (e, a, b) in ascending
+//      (e, a, b) order (slot_ptr + codes, code = sym(a,b) * n_local + e_local).
+#include <climits>
+#include <vector>
+
+#include "lfem_internal.cuh"
+
+namespace {
+
+constexpr int MAX_CAND = 512;   // candidate (element, column) entries per row
+constexpr int ROW_WARPS = 8;    // warps per block in k_row_pattern
+
+__global__ void k_flag(const int32_t* __restrict__ conn, int64_t n_elems, int nref, int64_t rb, int64_t re,
+                       int32_t* __restrict__ flag) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_elems;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        int f = 0;
+        for (int a = 0; a < nref; ++a) {
+            const int64_t v = conn[e * nref + a];
+            f |= (v >= rb && v < re);
+        }
+        flag[e] = f;
+    }
+}
+
+__global__ void k_compact(const int32_t* __restrict__ flag, const int64_t* __restrict__ pos, int64_t n_elems,
+                          const int32_t* __restrict__ conn, int nref, int32_t* __restrict__ elem_list,
+                          int32_t* __restrict__ local_conn) {
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n_elems;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        if (flag[e]) {
+            const int64_t le = pos[e];
+            elem_list[le] = (int32_t)e;
+            for (int a = 0; a < nref; ++a) local_conn[le * nref + a] = conn[e * nref + a];
+        }
+    }
+}
+
+__global__ void k_count(const int32_t* __restrict__ lconn, int64_t n_local, int nref, int64_t rb, int64_t re,
+                        int32_t* __restrict__ cnt) {
+    const int64_t n = n_local * nref;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = lconn[i];
+        if (r >= rb && r < re) atomicAdd(&cnt[r - rb], 1);
+    }
+}
+
+__global__ void k_fill(const int32_t* __restrict__ lconn, int64_t n_local, int nref, int64_t rb, int64_t re,
+                       const int64_t* __restrict__ inc_ptr, int32_t* __restrict__ cursor, int32_t* __restrict__ inc) {
+    const int64_t n = n_local * nref;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = lconn[i];
+        if (r >= rb && r < re) {
+            const int k = atomicAdd(&cursor[r - rb], 1);
+            inc[inc_ptr[r - rb] + k] = (int32_t)i;  // i = e_local * nref + a
+        }
+    }
+}
+
+// insertion sort of each row's incidence list (segments are short: <= 51)
+__global__ void k_sort_inc(const int64_t* __restrict__ inc_ptr, int64_t n_rows, int32_t* __restrict__ inc) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = inc_ptr[r], e = inc_ptr[r + 1];
+        for (int64_t i = b + 1; i < e; ++i) {
+            const int32_t v = inc[i];
+            int64_t j = i - 1;
+            while (j >= b && inc[j] > v) {
+                inc[j + 1] = inc[j];
+                --j;
+            }
+            inc[j + 1] = v;
+        }
+    }
+}
+
+// One warp per row.  PASS 0: row_len.  PASS 1: col_idx, slot_ptr, codes.
+template <int PASS>
+__global__ void __launch_bounds__(ROW_WARPS * 32)
+k_row_pattern(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc, int64_t n_rows,
+              const int32_t* __restrict__ lconn, int nref, int64_t n_local, int32_t* __restrict__ row_len,
+              const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx, int32_t* __restrict__ slot_ptr,
+              int32_t* __restrict__ codes, int* __restrict__ overflow) {
+    __shared__ int32_t s_col[ROW_WARPS][MAX_CAND];
+    __shared__ int32_t s_src[ROW_WARPS][MAX_CAND];  // e_local * nref + a  (PASS 1)
+    __shared__ uint8_t s_first[ROW_WARPS][MAX_CAND];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * ROW_WARPS;
+    for (int64_t r = blockIdx.x * (int64_t)ROW_WARPS + warp; r < n_rows; r += nwarps) {
+        const int64_t ib = inc_ptr[r], ie = inc_ptr[r + 1];
+        const int nc = (int)((ie - ib) * nref);
+        if (nc > MAX_CAND) {
+            if (lane == 0) atomicExch(overflow, 1);
+            if (PASS == 0 && lane == 0) row_len[r] = 0;
+            continue;
+        }
+        for (int i = lane; i < nc; i += 32) {
+            const int k = i / nref, b = i - k * nref;
+            const int32_t src = inc[ib + k];
+            const int32_t le = src / nref;
+            s_col[warp][i] = lconn[(int64_t)le * nref + b];
+            s_src[warp][i] = src;
+        }
+        __syncwarp();
+        if (PASS == 0) {
+            int nfirst = 0;
+            for (int i = lane; i < nc; i += 32) {
+                const int32_t c = s_col[warp][i];
+                bool first = true;
+                for (int j = 0; j < i; ++j) first &= (s_col[warp][j] != c);
+                nfirst += first;
+            }
+            for (int o = 16; o > 0; o >>= 1) nfirst += __shfl_down_sync(0xffffffffu, nfirst, o);
+            if (lane == 0) row_len[r] = nfirst;
+        } else {
+            for (int i = lane; i < nc; i += 32) {
+                const int32_t c = s_col[warp][i];
+                bool first = true;
+                for (int j = 0; j < i; ++j) first &= (s_col[warp][j] != c);
+                s_first[warp][i] = first;
+            }
+            __syncwarp();
+            const int64_t rp = row_ptr[r];
+            const int64_t cbase = ib * nref;  // contributions of row r start here
+            for (int i = lane; i < nc; i += 32) {
+                const int32_t c = s_col[warp][i];
+                int less = 0, less_unique = 0, before_eq = 0;
+                for (int j = 0; j < nc; ++j) {
+                    const int32_t cj = s_col[warp][j];
+                    less += (cj < c);
+                    less_unique += (cj < c) & s_first[warp][j];
+                    before_eq += (cj == c) & (j < i);
+                }
+                if (s_first[warp][i]) {
+                    col_idx[rp + less_unique] = c;
+                    slot_ptr[rp + less_unique] = (int32_t)(cbase + less);
+                }
+                const int32_t src = s_src[warp][i];
+                const int32_t le = src / nref;
+                const int a = src - le * nref;
+                const int b = i - (i / nref) * nref;
+                codes[cbase + less + before_eq] = (int32_t)((int64_t)sym_index(nref, a, b) * n_local + le);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_set_last(int32_t* slot_ptr, int64_t nnz, int64_t total) { slot_ptr[nnz] = (int32_t)total; }
+
+inline unsigned grid_for(int64_t n, int threads) {
+    int64_t g = (n + threads - 1) / threads;
+    if (g < 1) g = 1;
+    if (g > 148 * 64) g = 148 * 64;
+    return (unsigned)g;
+}
+
+}  // namespace
+
+lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
+    const lfem_mesh_s* m = p->mesh;
+    const int nref = m->nref;
+    const int64_t rb = p->row_begin, re = p->row_end, n_rows = re - rb;
+    p->n_rows = n_rows;
+    // 1. elements touching the owned rows
+    int32_t* flag = nullptr;
+    int64_t* pos = nullptr;
+    LFEM_TRY(dev_alloc_t(&flag, m->n_elems + 1, s));
+    LFEM_TRY(dev_alloc_t(&pos, m->n_elems + 1, s));
+    if (m->n_elems > 0) {
+        k_flag<<<grid_for(m->n_elems, 256), 256, 0, s>>>(m->conn, m->n_elems, nref, rb, re, flag);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    LFEM_TRY(scan_exclusive_i32_to_i64(flag, pos, m->n_elems, s));
+    int64_t n_local = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&n_local, pos + m->n_elems, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    p->n_local = n_local;
+    if (n_local * (int64_t)nref * nref >= (int64_t)INT_MAX)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "n_elems_local * nref^2 >= 2^31");
+    LFEM_TRY(dev_alloc_t(&p->elem_list, n_local + 1, s));
+    LFEM_TRY(dev_alloc_t(&p->local_conn, n_local * nref + 1, s));
+    if (m->n_elems > 0) {
+        k_compact<<<grid_for(m->n_elems, 256), 256, 0, s>>>(flag, pos, m->n_elems, m->conn, nref, p->elem_list,
+                                                            p->local_conn);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    dev_free(flag, s);
+    dev_free(pos, s);
+    // 2. counting sort of local rows by global row
+    int32_t* cnt = nullptr;
+    int64_t* inc_ptr = nullptr;
+    LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
+    LFEM_TRY(dev_alloc_t(&inc_ptr, n_rows + 1, s));
+    LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
+    if (n_local > 0) {
+        k_count<<<grid_for(n_local * nref, 256), 256, 0, s>>>(p->local_conn, n_local, nref, rb, re, cnt);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    LFEM_TRY(scan_exclusive_i32_to_i64(cnt, inc_ptr, n_rows, s));
+    int64_t total_inc = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&total_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    p->n_contrib = total_inc * nref;
+    if (p->n_contrib >= (int64_t)INT_MAX)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "contributions >= 2^31");
+    int32_t* inc = nullptr;
+    LFEM_TRY(dev_alloc_t(&inc, total_inc + 1, s));
+    LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
+    if (n_local > 0) {
+        k_fill<<<grid_for(n_local * nref, 256), 256, 0, s>>>(p->local_conn, n_local, nref, rb, re, inc_ptr, cnt, inc);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    if (n_rows > 0) {
+        k_sort_inc<<<grid_for(n_rows, 128), 128, 0, s>>>(inc_ptr, n_rows, inc);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    // 3. row lengths
+    int* overflow = nullptr;
+    LFEM_TRY(dev_alloc_t(&overflow, 1, s));
+    LFEM_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int), s));
+    const unsigned rgrid = grid_for(n_rows, ROW_WARPS);
+    if (n_rows > 0) {
+        k_row_pattern<0><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, n_local, cnt,
+                                                          nullptr, nullptr, nullptr, nullptr, overflow);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    LFEM_TRY(dev_alloc_t(&p->row_ptr, n_rows + 1, s));
+    LFEM_TRY(scan_exclusive_i32_to_i64(cnt, p->row_ptr, n_rows, s));
+    int h_overflow = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&p->nnz, p->row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaMemcpyAsync(&h_overflow, overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    if (h_overflow)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row has more than 512 candidate (element, column) entries");
+    if (p->nnz >= (int64_t)INT_MAX) return lfem_fail(LFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
+    // 4. columns + reduction plan
+    LFEM_TRY(dev_alloc_t(&p->col_idx, p->nnz + 1, s));
+    LFEM_TRY(dev_alloc_t(&p->slot_ptr, p->nnz + 1, s));
+    LFEM_TRY(dev_alloc_t(&p->codes, p->n_contrib + 1, s));
+    if (n_rows > 0) {
+        k_row_pattern<1><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, n_local,
+                                                          nullptr, p->row_ptr, p->col_idx, p->slot_ptr, p->codes,
+                                                          overflow);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    k_set_last<<<1, 1, 0, s>>>(p->slot_ptr, p->nnz, p->n_contrib);
+    LFEM_CUDA(cudaGetLastError());
+    dev_free(cnt, s);
+    dev_free(inc_ptr, s);
+    dev_free(inc, s);
+    dev_free(overflow, s);
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    return LFEM_OK;
+}
+
+void free_tiles(TilePlan& t, cudaStream_t s) {
+    dev_free(t.tile_elem_ptr, s);
+    dev_free(t.tile_elems, s);
+    dev_free(t.tile_conn_ptr, s);
+    dev_free(t.tile_conn, s);
+    dev_free(t.tile_info, s);
+    dev_free(t.tile_code_ptr, s);
+    dev_free(t.codes16, s);
+    dev_free(t.slot_cnt, s);
+    t = TilePlan();
+}

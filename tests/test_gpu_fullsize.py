@@ -1,0 +1,115 @@
+"""GPU parity at BASELINE.json's full sizes (C2..C5), in the launch
+configuration bench.py times: sampled rows against the oracle (computed row
+by row), plus properties that hold at any size (A 1 = 0, 1^T M 1, trace
+identities) evaluated with the library's own SpMV over every row."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import lfem_inputs as li
+import oracle
+from gpu_common import TOL, sample_rows
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a GPU", allow_module_level=True)
+
+from paper_2605_14035_b200 import lfem  # noqa: E402
+
+KINDS = {"C2": ("M", "A"), "C3": ("M", "Aa"), "C4": ("M", "A"), "C5": ("M", "A", "Aa")}
+
+
+def _run(name, coeff=None):
+    m = li.make_config(name)
+    kinds = KINDS[name]
+    plan, row_ptr, col_idx, vals = lfem.assemble(m, kinds, coeff=coeff)
+    return m, kinds, plan, row_ptr, col_idx, vals
+
+
+def _check_sampled(m, kinds, row_ptr, col_idx, vals, coeff, nsample=1500):
+    rows = sample_rows(m.n_nodes, nsample, seed=hash(m.extra["name"]) % 1000)
+    o = oracle.assemble_rows(m, kinds, rows=rows, coeff=coeff)
+    rp = row_ptr.cpu().numpy()
+    starts, ends = rp[rows], rp[rows + 1]
+    idx = np.concatenate([np.arange(a, b) for a, b in zip(starts, ends)])
+    idx_t = torch.as_tensor(idx, device="cuda")
+    g_col = col_idx[idx_t].cpu().numpy()
+    g_vals = {k: v[idx_t].cpu().numpy() for k, v in vals.items()}
+    g_rp = np.concatenate([[0], np.cumsum(ends - starts)])
+    assert np.array_equal(g_rp, o.row_ptr)
+    assert np.array_equal(g_col, o.col_idx)
+    worst = 0.0
+    for j in range(rows.size):
+        s, e = o.row_ptr[j], o.row_ptr[j + 1]
+        for k in kinds:
+            ov = o.vals[k][s:e]
+            err = np.abs(g_vals[k][s:e] - ov).max()
+            scale = np.abs(ov).max()
+            assert err <= TOL * scale, (k, rows[j], err, scale)
+            worst = max(worst, err / scale)
+    return worst
+
+
+def _spmv(plan, v, x):
+    y = torch.empty(plan.n_rows, dtype=torch.float64, device="cuda")
+    lfem.lfem_spmv(plan, v, x, y)
+    return y
+
+
+def _properties(m, kinds, plan, vals, coeff, dim):
+    one = torch.ones(m.n_nodes, dtype=torch.float64, device="cuda")
+    mass = float(torch.dot(one, _spmv(plan, vals["M"], one)))
+    X = torch.as_tensor(m.coords, device="cuda")
+    for k in kinds:
+        if k == "M":
+            continue
+        r1 = _spmv(plan, vals[k], one)
+        # rowmax via segment max on the host-side row ids
+        assert float(r1.abs().max()) <= 1e-11 * float(vals[k].abs().max()), k
+    if "A" in kinds:
+        tr = sum(float(torch.dot(X[:, c].contiguous(), _spmv(plan, vals["A"], X[:, c].contiguous()))) for c in range(3))
+        # 4.8e8-term dot products of O(1) entries: rounding ~1e-10 relative
+        assert abs(tr / mass - dim) < 5e-9
+    if "Aa" in kinds:
+        u = torch.as_tensor(coeff, device="cuda")
+        uMu = float(torch.dot(u, _spmv(plan, vals["M"], u)))
+        tra = sum(float(torch.dot(X[:, c].contiguous(), _spmv(plan, vals["Aa"], X[:, c].contiguous())))
+                  for c in range(3))
+        assert abs(tra / (dim * (mass + uMu)) - 1.0) < 5e-9
+    return mass
+
+
+def test_C2_full_properties():
+    m, kinds, plan, rp, ci, vals = _run("C2")
+    _check_sampled(m, kinds, rp, ci, vals, None)
+    mass = _properties(m, kinds, plan, vals, None, 2)
+    assert abs(mass - 4 * math.pi) < 2e-9  # L7 P2 area error ~1.2e-9 (EOC 4)
+
+
+def test_C3_full_reps_0_and_99():
+    m = li.make_config("C3")
+    for t in (0, 99):
+        u = li.coeff_at_rep(m, t)
+        plan, rp, ci, vals = lfem.assemble(m, KINDS["C3"], coeff=u)
+        _check_sampled(m, KINDS["C3"], rp, ci, vals, u)
+        _properties(m, KINDS["C3"], plan, vals, u, 2)
+        del plan, vals
+        torch.cuda.empty_cache()
+
+
+def test_C4_full():
+    m, kinds, plan, rp, ci, vals = _run("C4")
+    _check_sampled(m, kinds, rp, ci, vals, None)
+    vol = _properties(m, kinds, plan, vals, None, 3)
+    assert abs(vol - 1.0) < 1e-11  # reading G16: |Omega_h| = 1
+
+
+def test_C5_full():
+    m, kinds, plan, rp, ci, vals = _run("C5")
+    assert plan.nnz == 482344962 and plan.n_rows == 41943042
+    _check_sampled(m, kinds, rp, ci, vals, m.coeff)
+    mass = _properties(m, kinds, plan, vals, m.coeff, 2)
+    assert abs(mass - 4 * math.pi) < 1e-9

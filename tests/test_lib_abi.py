@@ -1,0 +1,62 @@
+"""CPU checks of the C-ABI library: it builds for sm_100a, loads, and exports
+every function include/lfem.h declares (no compute calls without a GPU)."""
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def libpath():
+    from paper_2605_14035_b200 import build
+    return build.build()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "lfem.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(lfem_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ("lfem_mesh_create", "lfem_assemble_symbolic", "lfem_assemble_numeric", "lfem_csr_get"):
+        assert required in names
+
+
+def test_library_exports_every_declared_symbol(libpath):
+    lib = ctypes.CDLL(libpath)
+    missing = [n for n in declared_functions() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_binding_names_match_header():
+    from paper_2605_14035_b200 import lfem
+    assert set(lfem.EXPORTED) == set(declared_functions())
+    for n in declared_functions():
+        if n not in ("lfem_mesh_destroy", "lfem_plan_destroy", "lfem_error_element", "lfem_last_error"):
+            assert hasattr(lfem, n), n
+
+
+def test_sass_is_sm100a(libpath):
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", libpath], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2605_14035_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in txt and "from oracle" not in txt and "lfem_oracle" not in txt, f
+
+
+def test_version_without_gpu(libpath):
+    lib = ctypes.CDLL(libpath)
+    lib.lfem_version.restype = ctypes.c_char_p
+    assert b"sm_100a" in lib.lfem_version()
