@@ -1,5 +1,7 @@
 // Per-element fp64 geometry + local matrices (symmetric halves) for the
-// numeric kernels.  Included by numeric.cu after reference.cuh.
+// numeric kernels.  Included by numeric.cu after reference.cuh.  Both numeric
+// variants (V0 and TILED) call exactly these functions, so they produce the
+// same bits.
 //
 // Mathematics (§3.2, Listing 1):
 //   J(xi) = DF(xi) = sum_{j>=2} (x_j - x_1) grad_ref phi_j(xi)^T   (Eq. jacobian_inv P:317-327;
@@ -15,11 +17,17 @@
 //            A_loc(a,b) = sum_q (w_q / mu_q) (cof grad_a) . (cof grad_b)
 //   M_loc(a,b)  = sum_q w_q mu_q phi_a phi_b                    (Eq. P:346)
 //   Aa_loc(a,b) = sum_q a(u_h(xi_q)) * (stiffness integrand),  a(u) = 1 + u^2
-// Evaluation order ("scalars first"): the quadrature loop produces a few
-// scalars per point (w mu, K, a); the nsym entries are then contractions of
-// those scalars with the constant tables pp / gg -- few live registers, no
-// accumulator arrays.  Bulk stiffness keeps per-entry accumulators (the
-// gradient form is cheaper than the 6-entry metric form for tets).
+//                 (BASELINE.json north_star; reading G10: a evaluated at u_h(xi_q))
+//
+// Structure ("geometry once, one kind at a time"): geometry() turns the
+// element's nodes into a few scalars per quadrature point (w mu, K, a); each
+// kind is then a separate contraction of those scalars with the constant
+// tables pp / gg, emitting the nsym entries of that kind.  The tiled kernel
+// stages one kind at a time in shared memory (3x smaller stage than staging
+// all kinds together, numeric_tiled.cuh).  Reference-gradient components that
+// are identically zero (e.g. d phi_2 / d xi_2 for P2) are skipped at compile
+// time.  Bulk stiffness uses the gradient form per quadrature point (cheaper
+// than the 6-entry metric form for tets) and recomputes J per kind.
 #pragma once
 #include "lfem_internal.cuh"
 #include "reference.cuh"
@@ -49,6 +57,18 @@ struct Shape {
         if (j < NV) return 4 * g(j, n) * g(j, m);
         const int e = j - NV, i = ei(e), k = ej(e);
         return 4 * (g(i, n) * g(k, m) + g(k, n) * g(i, m));
+    }
+    // d phi_j / d xi_m vanishes identically
+    __host__ __device__ static constexpr bool DZ(int j, int m) {
+        bool z = SA(j, m) == 0;
+        for (int n = 0; n < D; ++n) z = z && SB(j, m, n) == 0;
+        return z;
+    }
+    // surface metric-form product gg[s][c] (c: 11, 12+21, 22) vanishes identically
+    __host__ __device__ static constexpr bool GGZ(int a, int b, int c) {
+        return c == 0 ? (DZ(a, 0) || DZ(b, 0))
+                      : c == 2 ? (DZ(a, 1 % D) || DZ(b, 1 % D))
+                               : ((DZ(a, 0) || DZ(b, 1 % D)) && (DZ(a, 1 % D) || DZ(b, 0)));
     }
 };
 
@@ -91,13 +111,25 @@ struct QuadXi {
 };
 __constant__ QuadXi c_xi[4];
 
-template <int F, bool DM, bool DA, bool DAA>
-struct Element {
+enum Kind { KIND_M = 0, KIND_A = 1, KIND_AA = 2 };
+
+template <int F>
+struct Elem {
     static constexpr int N = FamInfo<F>::NREF, D = FamInfo<F>::D, NQ = FamInfo<F>::NQ, NS = FamInfo<F>::NSYM;
     using S = typename FamShape<F>::S;
     static_assert(S::N == N, "shape table");
 
-    // J0[c][m], J1[c][m][n] (n >= m used; symmetric) from differences d_j = x_j - x_1
+    // Per-element scalars handed from geometry() to the kind contractions.
+    //  surface: w mu, K = (w / mu) adj(G) (3 entries) and a(u_h) per point;
+    //  bulk:    w mu and a(u_h) per point + the Jacobian parts J0, J1.
+    struct Geo {
+        double wmu[NQ];
+        double k11[D == 2 ? NQ : 1], k12[D == 2 ? NQ : 1], k22[D == 2 ? NQ : 1];
+        double aq[NQ];
+        double J0[3][D], J1[3][D][D];  // bulk only (unused on surfaces)
+    };
+
+    // J0[c][m], J1[c][m][n] from differences d_j = x_j - x_1
     static __device__ __forceinline__ void jac_parts(const double (&X)[N][3], double (&J0)[3][D],
                                                      double (&J1)[3][D][D]) {
 #pragma unroll
@@ -140,132 +172,158 @@ struct Element {
             }
     }
 
-    // Computes all requested symmetric local entries and hands each to
-    // sink(kind 0/1/2, s, value) exactly once.  Returns false if mu <= 0 or
-    // non-finite at some quadrature point.
-    template <class Sink>
-    static __device__ __forceinline__ bool compute(const double (&X)[N][3], const double (&U)[N], Sink& sink) {
+    // cofactor matrix C (C[k][m] = d det J / d J[k][m]) and det J (bulk)
+    static __device__ __forceinline__ double cof(const double (&J)[3][D], double (&C)[3][3]) {
+        C[0][0] = J[1][1 % D] * J[2][2 % D] - J[1][2 % D] * J[2][1 % D];
+        C[0][1] = J[1][2 % D] * J[2][0] - J[1][0] * J[2][2 % D];
+        C[0][2] = J[1][0] * J[2][1 % D] - J[1][1 % D] * J[2][0];
+        C[1][0] = J[0][2 % D] * J[2][1 % D] - J[0][1 % D] * J[2][2 % D];
+        C[1][1] = J[0][0] * J[2][2 % D] - J[0][2 % D] * J[2][0];
+        C[1][2] = J[0][1 % D] * J[2][0] - J[0][0] * J[2][1 % D];
+        C[2][0] = J[0][1 % D] * J[1][2 % D] - J[0][2 % D] * J[1][1 % D];
+        C[2][1] = J[0][2 % D] * J[1][0] - J[0][0] * J[1][2 % D];
+        C[2][2] = J[0][0] * J[1][1 % D] - J[0][1 % D] * J[1][0];
+        return J[0][0] * C[0][0] + J[0][1 % D] * C[0][1] + J[0][2 % D] * C[0][2];
+    }
+
+    // Geometry of one element; returns false if mu <= 0 or non-finite at some
+    // quadrature point (S:240 / S:294 analogue, reading G25).
+    template <bool COEF>
+    static __device__ __forceinline__ bool geometry(const double (&X)[N][3], const double (&U)[N], Geo& g) {
         const RefTab<F>& T = tab<F>();
         double J0[3][D], J1[3][D][D];
         jac_parts(X, J0, J1);
         bool ok = true;
-        if (D == 2) {
-            double wmu[NQ], k11[NQ], k12[NQ], k22[NQ], aq[NQ];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                double J[3][D];
-                jac_at(J0, J1, q, J);
+        for (int q = 0; q < NQ; ++q) {
+            double J[3][D];
+            jac_at(J0, J1, q, J);
+            if constexpr (D == 2) {
                 const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
                 const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
                 const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
                 const double det = g11 * g22 - g12 * g12;
                 ok &= (det > 0.0) & (det < INFINITY);
                 const double r = rsqrt_nr(det);
-                wmu[q] = T.w[q] * (det * r);
+                g.wmu[q] = T.w[q] * (det * r);
                 const double c = T.w[q] * r;
-                k11[q] = c * g22;
-                k12[q] = -c * g12;
-                k22[q] = c * g11;
-                if (DAA) {
-                    double u = 0.0;
-#pragma unroll
-                    for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
-                    aq[q] = fma(u, u, 1.0);
-                }
-            }
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                if (DM) {
-                    double m = 0.0;
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) m = fma(wmu[q], T.pp[q][s], m);
-                    sink(0, s, m);
-                }
-                if (DA || DAA) {
-                    double a = 0.0, aa = 0.0;
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) {
-                        double st = k11[q] * T.gg[q][s][0];
-                        st = fma(k12[q], T.gg[q][s][1], st);
-                        st = fma(k22[q], T.gg[q][s][2], st);
-                        if (DA) a += st;
-                        if (DAA) aa = fma(aq[q], st, aa);
-                    }
-                    if (DA) sink(1, s, a);
-                    if (DAA) sink(2, s, aa);
-                }
-            }
-        } else {
-            double wmu[NQ];
-            double A[(DA ? NS : 1)], Aa[(DAA ? NS : 1)];
-#pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                if (DA) A[s] = 0.0;
-                if (DAA) Aa[s] = 0.0;
-            }
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                double J[3][D];
-                jac_at(J0, J1, q, J);
+                g.k11[D == 2 ? q : 0] = c * g22;
+                g.k12[D == 2 ? q : 0] = -c * g12;
+                g.k22[D == 2 ? q : 0] = c * g11;
+            } else {
                 double C[3][3];
-                C[0][0] = J[1][1 % D] * J[2][2 % D] - J[1][2 % D] * J[2][1 % D];
-                C[0][1] = J[1][2 % D] * J[2][0] - J[1][0] * J[2][2 % D];
-                C[0][2] = J[1][0] * J[2][1 % D] - J[1][1 % D] * J[2][0];
-                C[1][0] = J[0][2 % D] * J[2][1 % D] - J[0][1 % D] * J[2][2 % D];
-                C[1][1] = J[0][0] * J[2][2 % D] - J[0][2 % D] * J[2][0];
-                C[1][2] = J[0][1 % D] * J[2][0] - J[0][0] * J[2][1 % D];
-                C[2][0] = J[0][1 % D] * J[1][2 % D] - J[0][2 % D] * J[1][1 % D];
-                C[2][1] = J[0][2 % D] * J[1][0] - J[0][0] * J[1][2 % D];
-                C[2][2] = J[0][0] * J[1][1 % D] - J[0][1 % D] * J[1][0];
-                const double det = J[0][0] * C[0][0] + J[0][1 % D] * C[0][1] + J[0][2 % D] * C[0][2];
-                const double adet = fabs(det);
+                const double adet = fabs(cof(J, C));
                 ok &= (adet > 0.0) & (adet < INFINITY);
-                wmu[q] = T.w[q] * adet;
-                if (DA || DAA) {
-                    const double c = T.w[q] * rcp_nr(adet);
-                    double aq = 1.0;
-                    if (DAA) {
-                        double u = 0.0;
-#pragma unroll
-                        for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
-                        aq = fma(u, u, 1.0);
-                    }
-                    double g[N][3], h[N][3];
-#pragma unroll
-                    for (int a = 0; a < N; ++a)
-#pragma unroll
-                        for (int k = 0; k < 3; ++k) {
-                            double acc = C[k][0] * T.dphi[q][a][0];
-                            acc = fma(C[k][1], T.dphi[q][a][1 % D], acc);
-                            acc = fma(C[k][2], T.dphi[q][a][2 % D], acc);
-                            g[a][k] = acc;
-                            h[a][k] = c * acc;
-                        }
-#pragma unroll
-                    for (int a = 0; a < N; ++a)
-#pragma unroll
-                        for (int b = a; b < N; ++b) {
-                            const int s = sym_index(N, a, b);
-                            double st = h[a][0] * g[b][0];
-                            st = fma(h[a][1], g[b][1], st);
-                            st = fma(h[a][2], g[b][2], st);
-                            if (DA) A[s] += st;
-                            if (DAA) Aa[s] = fma(aq, st, Aa[s]);
-                        }
-                }
+                g.wmu[q] = T.w[q] * adet;
             }
+            if (COEF) {
+                double u = 0.0;
 #pragma unroll
-            for (int s = 0; s < NS; ++s) {
-                if (DM) {
-                    double m = 0.0;
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q) m = fma(wmu[q], T.pp[q][s], m);
-                    sink(0, s, m);
-                }
-                if (DA) sink(1, s, A[s]);
-                if (DAA) sink(2, s, Aa[s]);
+                for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
+                g.aq[q] = fma(u, u, 1.0);
             }
         }
+        if constexpr (D == 3) {
+#pragma unroll
+            for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                for (int m = 0; m < D; ++m) {
+                    g.J0[cc][m] = J0[cc][m];
+#pragma unroll
+                    for (int n = 0; n < D; ++n) g.J1[cc][m][n] = J1[cc][m][n];
+                }
+        }
         return ok;
+    }
+
+    // M_loc(s) = sum_q w_q mu_q phi_a phi_b   -> sink(s, value), s ascending.
+    // Quadrature loop outside, entries inside: nsym independent accumulation
+    // chains (ILP); each entry still sums its terms in ascending q.
+    template <class Sink>
+    static __device__ __forceinline__ void mass(const Geo& g, Sink& sink) {
+        const RefTab<F>& T = tab<F>();
+        double m[NS];
+#pragma unroll
+        for (int s = 0; s < NS; ++s) m[s] = 0.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+#pragma unroll
+            for (int s = 0; s < NS; ++s) m[s] = fma(g.wmu[q], T.pp[q][s], m[s]);
+#pragma unroll
+        for (int s = 0; s < NS; ++s) sink(s, m[s]);
+    }
+
+    // A_loc (COEF = false) or A_a,loc (COEF = true) -> sink(s, value)
+    template <bool COEF, class Sink>
+    static __device__ __forceinline__ void stiffness(const Geo& g, Sink& sink) {
+        const RefTab<F>& T = tab<F>();
+        if constexpr (D == 2) {
+            double c11[NQ], c12[NQ], c22[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                c11[q] = COEF ? g.aq[q] * g.k11[D == 2 ? q : 0] : g.k11[D == 2 ? q : 0];
+                c12[q] = COEF ? g.aq[q] * g.k12[D == 2 ? q : 0] : g.k12[D == 2 ? q : 0];
+                c22[q] = COEF ? g.aq[q] * g.k22[D == 2 ? q : 0] : g.k22[D == 2 ? q : 0];
+            }
+            double v[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) v[s] = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q)
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = a; b < N; ++b) {
+                        const int s = sym_index(N, a, b);
+                        if (!S::GGZ(a, b, 0)) v[s] = fma(c11[q], T.gg[q][s][0], v[s]);
+                        if (!S::GGZ(a, b, 1)) v[s] = fma(c12[q], T.gg[q][s][1], v[s]);
+                        if (!S::GGZ(a, b, 2)) v[s] = fma(c22[q], T.gg[q][s][2], v[s]);
+                    }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) sink(s, v[s]);
+        } else {
+            double acc[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                double J[3][D], C[3][3];
+                jac_at(g.J0, g.J1, q, J);
+                const double adet = fabs(cof(J, C));
+                double c = T.w[q] * rcp_nr(adet);
+                if (COEF) c = c * g.aq[q];
+                double gr[N][3], h[N][3];
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) {
+                        double v = 0.0;
+#pragma unroll
+                        for (int m = 0; m < D; ++m)
+                            if (!S::DZ(a, m)) v = fma(C[k][m], T.dphi[q][a][m], v);
+                        gr[a][k] = v;
+                        h[a][k] = c * v;
+                    }
+#pragma unroll
+                for (int a = 0; a < N; ++a)
+#pragma unroll
+                    for (int b = a; b < N; ++b) {
+                        const int s = sym_index(N, a, b);
+                        double st = h[a][0] * gr[b][0];
+                        st = fma(h[a][1], gr[b][1], st);
+                        st = fma(h[a][2], gr[b][2], st);
+                        acc[s] = acc[s] + st;
+                    }
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) sink(s, acc[s]);
+        }
+    }
+
+    template <int KIND, class Sink>
+    static __device__ __forceinline__ void kind(const Geo& g, Sink& sink) {
+        if (KIND == KIND_M) mass(g, sink);
+        else if (KIND == KIND_A) stiffness<false>(g, sink);
+        else stiffness<true>(g, sink);
     }
 };

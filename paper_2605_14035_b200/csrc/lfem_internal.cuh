@@ -33,26 +33,22 @@ struct lfem_mesh_s {
     const int32_t* conn;
 };
 
-// Row-tile plan of the fused numeric kernel.
+// Row-tile plan of the fused numeric kernel (tiles.cu).
 struct TilePlan {
     int n_tiles = 0;
-    int rows_per_tile = 0;
-    int max_tile_elems = 0;     // max elements per tile (smem sizing)
-    int max_tile_slots = 0;
-    int max_tile_codes = 0;
-    int built_nk = 0;                   // kinds count the tile size was chosen for
-    int32_t* tile_elem_ptr = nullptr;   // n_tiles + 1 (into tile_elems)
+    int rows_per_tile = 0;      // average rows per tile (tiles are built by element budget)
+    int max_tile_elems = 0;     // max elements per tile = stage stride (codes are sym * maxe + e_tile)
+    int max_tile_slots = 0;     // max CSR slots per tile
+    int max_tile_heavy = 0;     // max heavy-list u16 words per tile
+    int heavy_words = 8;        // u16 words per heavy entry (16-B multiple)
     int32_t* tile_elems = nullptr;      // plan-local element ids, ascending per tile
-    int32_t* tile_conn_ptr = nullptr;   // n_tiles + 1 (int32 offsets into tile_conn, multiples of 4)
-    int32_t* tile_conn = nullptr;       // per tile: its elements' connectivity in tile order
-    int4* tile_info = nullptr;          // 2 per tile: {s0, ns, c0, nc}, {e0, ne, q0, nq}
-    int32_t* tile_code_ptr = nullptr;   // n_tiles + 1 (into codes16)
-    uint16_t* codes16 = nullptr;        // per slot, per contribution: elem_in_tile*NSYM + sym
-    uint8_t* slot_cnt = nullptr;        // nnz: contributions per slot
-    size_t smem_bytes = 0;
+    int32_t* tile_conn = nullptr;       // per tile: its elements' connectivity in tile order (16-B padded)
+    int4* tile_info = nullptr;          // 2 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}
+    uint32_t* pairs = nullptr;          // nnz: per slot, (c0 | c1 << 16); c1 = 0xffff if one contribution;
+                                        // 0xffffffff for a heavy slot (> 2 contributions)
+    uint16_t* heavy = nullptr;          // per heavy slot: [slot - s0, count, codes...] (fixed size per family)
     bool ready = false;
 };
-
 struct Profiler;  // api.cu
 void prof_begin(lfem_plan_s* p, const char* name, cudaStream_t s);
 void prof_end(lfem_plan_s* p, cudaStream_t s);
@@ -108,7 +104,8 @@ lfem_status scan_exclusive_i32_to_i64(const int32_t* in, int64_t* out, int64_t n
 
 // symbolic.cu
 lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s);
-lfem_status build_tiles(lfem_plan_s* p, int rows_per_tile, cudaStream_t s);
+lfem_status build_incidence(lfem_plan_s* p, int64_t** inc_ptr, int32_t** inc, cudaStream_t s);
+lfem_status build_tiles(lfem_plan_s* p, int max_tile_elems, cudaStream_t s);
 void free_tiles(TilePlan& t, cudaStream_t s);
 
 // numeric.cu

@@ -32,13 +32,10 @@ namespace {
 // --------------------------------------------------------------------------
 // V0: element kernel -> stage[k][s][le]; slot kernel -> vals
 // --------------------------------------------------------------------------
-struct GlobalStageSink {
+struct GlobalStageSink {  // stage[s * n_local + le] of one kind
     double* stage;
     int64_t n_local, le;
-    __device__ __forceinline__ void operator()(int k, int s, double v) const {
-        stage[(int64_t)k * nsym_stride + (int64_t)s * n_local + le] = v;
-    }
-    int64_t nsym_stride;
+    __device__ __forceinline__ void operator()(int s, double v) const { stage[(int64_t)s * n_local + le] = v; }
 };
 
 template <int F, bool DM, bool DA, bool DAA>
@@ -46,7 +43,7 @@ __global__ void __launch_bounds__(128)
 k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __restrict__ elem_list,
           const double* __restrict__ coords, const double* __restrict__ coeff, double* __restrict__ stage,
           int* __restrict__ err) {
-    using E = Element<F, DM, DA, DAA>;
+    using E = Elem<F>;
     constexpr int N = E::N, NS = E::NS;
     for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < n_local;
          le += (int64_t)gridDim.x * blockDim.x) {
@@ -58,8 +55,21 @@ k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __r
             for (int c = 0; c < 3; ++c) X[a][c] = __ldg(&coords[3 * v + c]);
             U[a] = DAA ? __ldg(&coeff[v]) : 0.0;
         }
-        GlobalStageSink sink{stage, n_local, le, (int64_t)NS * n_local};
-        if (!E::compute(X, U, sink)) atomicMin(err, __ldg(&elem_list[le]));
+        typename E::Geo g;
+        if (!E::template geometry<DAA>(X, U, g)) atomicMin(err, __ldg(&elem_list[le]));
+        const int64_t stride = (int64_t)NS * n_local;
+        if (DM) {
+            GlobalStageSink sink{stage, n_local, le};
+            E::template kind<KIND_M>(g, sink);
+        }
+        if (DA) {
+            GlobalStageSink sink{stage + stride, n_local, le};
+            E::template kind<KIND_A>(g, sink);
+        }
+        if (DAA) {
+            GlobalStageSink sink{stage + 2 * stride, n_local, le};
+            E::template kind<KIND_AA>(g, sink);
+        }
     }
 }
 

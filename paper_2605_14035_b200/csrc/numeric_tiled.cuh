@@ -1,28 +1,38 @@
 // Fused row-tile numeric kernel (TILED variant) -- included by numeric.cu.
 //
-// One CTA per row tile (tiles.cu).  Per tile:
-//   0. one thread arms an mbarrier and issues TMA bulk copies
-//      (cp.async.bulk -> UBLKCP) of the tile's element connectivity (tile
-//      order), its 16-bit contribution codes and 8-bit slot counts into
-//      shared memory;
-//   A. each thread takes one tile element: node ids from shared memory,
-//      coordinates gathered from global (L2-resident: SFC order), local
-//      matrices in fp64 registers (Element<>), symmetric halves stored to the
-//      shared-memory stage  stage[kind][sym][e_tile];
-//   B. each warp owns a contiguous run of the tile's CSR slots; 32 slots at a
-//      time it scans their counts with shuffles, sums each slot's
-//      contributions in code order (= ascending element, reading G21) and
-//      stores vals[kind][slot] -- 32 consecutive slots per store instruction;
-//      no atomics.
-// HBM traffic per tile: CSR values (written once), 2 B per contribution code,
-// 1 B per slot count, the tile's connectivity, gathered coordinates.
+// Persistent, one CTA per SM, warp-specialised:
+//
+//   producer   (lane 0 of the first reduce warp): TMA bulk copies
+//              (cp.async.bulk -> UBLKCP) of a tile's metadata -- element
+//              connectivity (tile order), per-slot code words, heavy lists --
+//              into one of 3 shared-memory meta buffers, mbarrier-tracked,
+//              up to 3 tiles ahead.
+//   compute    CW warps, EPT elements per thread: prefetch node coordinates
+//              (and u) of the thread's elements of the NEXT tile into its own
+//              shared-memory slots (cp.async -> LDGSTS) while the current tile
+//              computes; fp64 geometry;
+//              then, one kind at a time (M, A, A_a), the nsym local entries
+//              into a shared-memory stage  stage[s * maxe + e_tile].
+//   reduce     RW warps: for each kind, every CSR slot of the tile sums its
+//              1..c contributions from the stage in symbolic order (ascending
+//              element, reading G21) and stores 32 consecutive slots per
+//              warp store (streaming, no atomics).
+//
+// The stage is double-buffered per kind: the reduce warps drain kind k of a
+// tile while the compute warps produce kind k+1 (or the next tile's
+// geometry), so HBM stores, L2 gathers and the FP64 pipe overlap inside one
+// SM.  Staging one kind at a time keeps the stage at nsym * 8 B per element
+// (168 B for P2 triangles), which is what lets a CTA hold ~256-element tiles
+// (halo recompute ~1.4x) with both buffers resident.
 #pragma once
+#include <cstdio>
 #include <cstdlib>
 
-#ifndef LFEM_P2T_THREADS
-#define LFEM_P2T_THREADS 192
-#define LFEM_P2T_MINB 2
-#define LFEM_P2T_R 256
+#ifndef LFEM_RW
+#define LFEM_RW 8
+#endif
+#ifndef LFEM_RU
+#define LFEM_RU 4
 #endif
 
 namespace {
@@ -35,6 +45,10 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
@@ -60,325 +74,448 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     } while (!done);
 }
 
+// per-role phase accounting (debug bit 2; timing experiments only)
+struct PhaseClock {
+    bool on;
+    long long t0;
+    __device__ __forceinline__ void start() { if (on) t0 = clock64(); }
+    __device__ __forceinline__ void lap(unsigned long long* acc, int k) {
+        if (on) { const long long t = clock64(); atomicAdd(&acc[k], (unsigned long long)(t - t0)); t0 = t; }
+    }
+};
+
+__device__ __forceinline__ void st_stream(double* p, double v) {
+    asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+
+// CW compute warps, RW reduce warps, EPT elements per compute thread (tile
+// element budget CW*32*EPT), RU light-slot chunks per reduce iteration,
+// REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default),
+// PRE: prefetch the next tile's nodes (cp.async) during the current tile.
+template <int F> struct TileCfg;
+template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 2, RU = LFEM_RU, REGS_C = 0, REGS_R = 0; static constexpr bool PRE = true; };
+template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_RW == 8 ? 168 : 0, REGS_R = LFEM_RW == 8 ? 88 : 0; static constexpr bool PRE = true; };
+template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; static constexpr bool PRE = false; };
+template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; static constexpr bool PRE = false; };
+
 struct TileLayout {
-    size_t buf_off[2], conn_off, codes_off, cnt_off, buf_bytes, heavy_off, soff_off, total;
+    size_t stage_bytes;           // one stage buffer
+    size_t meta_off[3], conn_off, pairs_off, heavy_off, meta_bytes, pre_off, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-// stage | 2 x {conn | codes | counts} | heavy-slot lists
-__host__ __device__ inline TileLayout tile_layout(int nk, int nsym, int nref, int maxe, int codes_cap, int slots_cap,
-                                                  int nwarps, int maxh) {
+// stage[2] | meta[3] = {conn | pairs | heavy}
+__host__ __device__ inline TileLayout tile_layout(int nsym, int nref, int maxe, int slots_cap, int heavy_cap,
+                                                  int pre_elems) {
     TileLayout L;
-    const size_t stage = align16(sizeof(double) * (size_t)nk * nsym * maxe);
+    L.stage_bytes = align16(sizeof(double) * (size_t)nsym * maxe);
     L.conn_off = 0;
-    L.codes_off = align16(sizeof(int32_t) * ((size_t)maxe * nref + 4));
-    L.cnt_off = L.codes_off + align16(sizeof(uint16_t) * ((size_t)codes_cap + 16));
-    L.buf_bytes = L.cnt_off + align16((size_t)slots_cap + 32);
-    L.buf_off[0] = stage;
-    L.buf_off[1] = stage + L.buf_bytes;
-    L.heavy_off = stage + 2 * L.buf_bytes;
-    L.soff_off = L.heavy_off + align16(sizeof(int) * 2 * (size_t)nwarps * maxh);
-    L.total = L.soff_off + align16(sizeof(uint16_t) * ((size_t)slots_cap + 8));
+    L.pairs_off = align16(sizeof(int32_t) * ((size_t)maxe * nref + 4));
+    L.heavy_off = L.pairs_off + align16(sizeof(uint32_t) * ((size_t)slots_cap + 8));
+    L.meta_bytes = L.heavy_off + align16(sizeof(uint16_t) * ((size_t)heavy_cap + 16));
+    for (int b = 0; b < 3; ++b) L.meta_off[b] = 2 * L.stage_bytes + b * L.meta_bytes;
+    L.pre_off = 2 * L.stage_bytes + 3 * L.meta_bytes;
+    L.total = L.pre_off + sizeof(double) * (size_t)4 * nref * pre_elems;  // pre[j][c][e]: x, y, z, u
     return L;
 }
 
 struct TileArgs {
     int n_tiles;
-    int maxe, codes_cap, slots_cap;
-    const int4* tile_info;
+    int maxe, slots_cap, heavy_cap, heavy_words;
+    const int4* tile_info;      // 2 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}
     const int32_t* tile_elems;
     const int32_t* tile_conn;
-    const uint16_t* codes16;
-    const uint8_t* slot_cnt;
+    const uint32_t* pairs;
+    const uint16_t* heavy;
     const int32_t* elem_list;
     const double* coords;
     const double* coeff;
     double* v[3];
     int* err;
-    int debug;  // timing experiments only (LFEM_DEBUG_TILED): bit0 skip phase A, bit1 skip phase B
+    int debug;  // timing experiments only (env LFEM_DEBUG_TILED): bit0 compute skips the kinds, bit1 reduce skips the slots,
+                //   bit2 per-role phase cycles -> dbg[16]
+    unsigned long long* dbg;
 };
 
 extern __shared__ __align__(16) double tile_smem_d[];  // dynamic shared memory (one view per TU)
 
-struct SmemStageSink {  // stage[kind][sym][e_tile] as offsets into tile_smem_d
-    int e, maxe, k1, k2;  // k1 = offset of kind A, k2 = offset of kind Aa (in doubles)
-    __device__ __forceinline__ void operator()(int k, int s, double v) const {
-        const int kofs = k == 0 ? 0 : (k == 1 ? k1 : k2);
-        tile_smem_d[kofs + s * maxe + e] = v;
-    }
+struct StageSink {  // stage[s * maxe + e]
+    double* st;
+    int maxe, e;
+    __device__ __forceinline__ void operator()(int s, double v) const { st[s * maxe + e] = v; }
 };
 
-// THREADS per CTA, MINB CTAs per SM, default rows per tile, LIGHT = slots with
-// at most LIGHT contributions are summed in the main (coalesced) pass, the
-// rest ("heavy": vertex diagonals) in a per-warp second pass; MAXH heavy
-// slots recorded per warp and tile.
-template <int F> struct TileCfg;
-template <> struct TileCfg<FAM_TRI_P1> { static constexpr int THREADS = 256, MINB = 2, R = 512, LIGHT = 2, MAXH = 96; };
-template <> struct TileCfg<FAM_TRI_P2> { static constexpr int THREADS = LFEM_P2T_THREADS, MINB = LFEM_P2T_MINB, R = LFEM_P2T_R, LIGHT = 2, MAXH = 64; };
-template <> struct TileCfg<FAM_TET_P1> { static constexpr int THREADS = 256, MINB = 1, R = 256, LIGHT = 4, MAXH = 96; };
-template <> struct TileCfg<FAM_TET_P2> { static constexpr int THREADS = 256, MINB = 1, R = 128, LIGHT = 4, MAXH = 96; };
-
-__device__ __forceinline__ int warp_incl_scan_i(int v, int lane) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    return v;
-}
-
-// thread 0: publish tile info for buffer b and start its TMA bulk copies
-__device__ __forceinline__ void issue_tile(const TileArgs& a, unsigned char* smem, const TileLayout& lay, int b,
-                                           int4 i0, int4 i1, int4 (*sinfo)[2], uint64_t* bar) {
+// producer: publish tile t's info in sinfo[b] and start its bulk copies into meta buffer b
+__device__ __forceinline__ void issue_tile(const TileArgs& a, unsigned char* smem, const TileLayout& lay, int t,
+                                           int b, int4 (*sinfo)[2], uint64_t* bar) {
+    const int4 i0 = a.tile_info[2 * t], i1 = a.tile_info[2 * t + 1];
     sinfo[b][0] = i0;
     sinfo[b][1] = i1;
-    unsigned char* buf = smem + lay.buf_off[b];
-    const uintptr_t cb = reinterpret_cast<uintptr_t>(a.codes16 + i0.z);
-    const uintptr_t ce = reinterpret_cast<uintptr_t>(a.codes16 + i0.z + i0.w);
-    const uintptr_t cb16 = cb & ~uintptr_t(15), ce16 = (ce + 15) & ~uintptr_t(15);
-    const uintptr_t nb = reinterpret_cast<uintptr_t>(a.slot_cnt + i0.x);
-    const uintptr_t nbe = reinterpret_cast<uintptr_t>(a.slot_cnt + i0.x + i0.y);
-    const uintptr_t nb16 = nb & ~uintptr_t(15), ne16 = (nbe + 15) & ~uintptr_t(15);
-    const uint32_t bytes_q = (uint32_t)i1.w * 4u;
-    const uint32_t bytes_c = (uint32_t)(ce16 - cb16), bytes_n = (uint32_t)(ne16 - nb16);
-    mbar_arrive_expect_tx(&bar[b], bytes_q + bytes_c + bytes_n);
-    if (bytes_q) bulk_g2s(buf + lay.conn_off, a.tile_conn + i1.z, bytes_q, &bar[b]);
-    if (bytes_c) bulk_g2s(buf + lay.codes_off, reinterpret_cast<const void*>(cb16), bytes_c, &bar[b]);
-    if (bytes_n) bulk_g2s(buf + lay.cnt_off, reinterpret_cast<const void*>(nb16), bytes_n, &bar[b]);
+    unsigned char* buf = smem + lay.meta_off[b];
+    const int p0 = i0.x & ~3, p1 = (i0.x + i0.y + 3) & ~3;    // u32, 16-B aligned
+    const int h0 = i1.z & ~7, h1 = (i1.z + i1.w + 7) & ~7;    // u16, 16-B aligned
+    const uint32_t bq = (uint32_t)i1.y * 4u, bp = (uint32_t)(p1 - p0) * 4u, bh = (uint32_t)(h1 - h0) * 2u;
+    mbar_arrive_expect_tx(&bar[b], bq + bp + bh);
+    if (bq) bulk_g2s(buf + lay.conn_off, a.tile_conn + i1.x, bq, &bar[b]);
+    if (bp) bulk_g2s(buf + lay.pairs_off, a.pairs + p0, bp, &bar[b]);
+    if (bh) bulk_g2s(buf + lay.heavy_off, a.heavy + h0, bh, &bar[b]);
 }
 
-// Persistent: CTA c processes tiles c, c + G, c + 2G, ...; the next tile's
-// connectivity / codes / counts stream into the other buffer while the
-// current tile computes and reduces.
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// The thread's elements e = ci + k*ct of a tile: node coordinates (and u) either
+// gathered straight into registers (load_nodes) or prefetched asynchronously
+// into the thread's own slots of pre[j][c][e] (prefetch_nodes, cp.async ->
+// LDGSTS; no registers held while in flight) and read back later (read_nodes).
+template <int F, bool COEF, int EPT>
+__device__ __forceinline__ void load_nodes(const TileArgs& a, const int32_t* s_conn, int ne, int ci, int ct,
+                                           double (&X)[EPT][FamInfo<F>::NREF][3], double (&U)[EPT][FamInfo<F>::NREF]) {
+    constexpr int N = FamInfo<F>::NREF;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int e = ci + k * ct;
+        if (e < ne) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const int64_t v = s_conn[e * N + j];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) X[k][j][c] = __ldg(&a.coords[3 * v + c]);
+                U[k][j] = COEF ? __ldg(&a.coeff[v]) : 0.0;
+            }
+        }
+    }
+}
+
+template <int F, bool COEF, int EPT>
+__device__ __forceinline__ void prefetch_nodes(const TileArgs& a, const int32_t* s_conn, int ne, int ci, int ct,
+                                               double* pre, int pe) {
+    constexpr int N = FamInfo<F>::NREF;
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int e = ci + k * ct;
+        if (e < ne) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+                const int64_t v = s_conn[e * N + j];
+#pragma unroll
+                for (int c = 0; c < 3; ++c) cp_async8(pre + (j * 4 + c) * pe + e, a.coords + 3 * v + c);
+                if (COEF) cp_async8(pre + (j * 4 + 3) * pe + e, a.coeff + v);
+            }
+        }
+    }
+    cp_async_commit();
+}
+
+template <int F, bool COEF, int EPT>
+__device__ __forceinline__ void read_nodes(const double* pre, int pe, int ne, int ci, int ct,
+                                           double (&X)[EPT][FamInfo<F>::NREF][3], double (&U)[EPT][FamInfo<F>::NREF]) {
+    constexpr int N = FamInfo<F>::NREF;
+    cp_async_wait_all();
+#pragma unroll
+    for (int k = 0; k < EPT; ++k) {
+        const int e = ci + k * ct;
+        if (e < ne) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) {
+#pragma unroll
+                for (int c = 0; c < 3; ++c) X[k][j][c] = pre[(j * 4 + c) * pe + e];
+                U[k][j] = COEF ? pre[(j * 4 + 3) * pe + e] : 0.0;
+            }
+        }
+    }
+}
+
 template <int F, bool DM, bool DA, bool DAA>
-__global__ void __launch_bounds__(TileCfg<F>::THREADS, TileCfg<F>::MINB) k_tiled(const TileArgs a) {
-    using E = Element<F, DM, DA, DAA>;
-    constexpr int N = E::N, NS = E::NS, TB = TileCfg<F>::THREADS, NW = TB / 32;
-    constexpr int LIGHT = TileCfg<F>::LIGHT, MAXH = TileCfg<F>::MAXH;
-    constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
+__global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_tiled(const TileArgs a) {
+    using E = Elem<F>;
+    using Cfg = TileCfg<F>;
+    constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
     unsigned char* smem = reinterpret_cast<unsigned char*>(tile_smem_d);
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int4 sinfo[2][2];
-    __shared__ int warp_sums[NW];
+    __shared__ __align__(8) uint64_t meta_full[3], meta_empty[3], stage_full[2], stage_empty[2];
+    __shared__ int4 sinfo[3][2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
-    const TileLayout lay = tile_layout(NK, NS, N, a.maxe, a.codes_cap, a.slots_cap, NW, MAXH);
-    // offsets (in doubles) of the kinds inside the stage
-    const int kst = NS * a.maxe;
-    const int ofsM = 0, ofsA = DM ? kst : 0, ofsAa = ((DM ? 1 : 0) + (DA ? 1 : 0)) * kst;
-    int* h_list = reinterpret_cast<int*>(smem + lay.heavy_off) + warp * 2 * MAXH;  // [slot, off] pairs
+    constexpr int PE = Cfg::PRE ? CW * 32 * EPT : 0;  // prefetch slots
+    const TileLayout lay = tile_layout(E::NS, N, a.maxe, a.slots_cap, a.heavy_cap, PE);
+    double* pre = reinterpret_cast<double*>(smem + lay.pre_off);
+    const int stage_dbl = (int)(lay.stage_bytes / sizeof(double));
 
-    int t = blockIdx.x;
-    int4 n0 = make_int4(0, 0, 0, 0), n1 = n0;  // thread 0: info of the next tile to issue
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        if (t < a.n_tiles) issue_tile(a, smem, lay, 0, a.tile_info[2 * t], a.tile_info[2 * t + 1], sinfo, bar);
-        if (t + G < a.n_tiles) {
-            n0 = a.tile_info[2 * (t + G)];
-            n1 = a.tile_info[2 * (t + G) + 1];
+        for (int b = 0; b < 3; ++b) {
+            mbar_init(&meta_full[b], 1);
+            mbar_init(&meta_empty[b], RW * 32);
         }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&stage_full[b], CT);
+            mbar_init(&stage_empty[b], RW * 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
+    if (tid == CT) {
+        for (int k = 0; k < 3; ++k) {
+            const int t = blockIdx.x + k * G;
+            if (t < a.n_tiles) issue_tile(a, smem, lay, t, k, sinfo, meta_full);
+        }
+    }
 
-    for (int it = 0; t < a.n_tiles; ++it, t += G) {
-        const int b = it & 1;
-        if (tid == 0 && t + G < a.n_tiles) {
-            issue_tile(a, smem, lay, b ^ 1, n0, n1, sinfo, bar);
-            if (t + 2 * G < a.n_tiles) {
-                n0 = a.tile_info[2 * (t + 2 * G)];
-                n1 = a.tile_info[2 * (t + 2 * G) + 1];
+    if (warp < CW) {
+        // ------------------------------------------------------------ compute warps
+        if (Cfg::REGS_C) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_C));
+        int t = blockIdx.x;
+        if (t >= a.n_tiles) return;
+        PhaseClock pc{(a.debug & 4) != 0 && tid == 0, 0};
+        pc.start();
+        double X[EPT][N][3], U[EPT][N];
+        uint32_t pass = 0;
+        if (Cfg::PRE) {
+            mbar_wait(&meta_full[0], 0);
+            prefetch_nodes<F, DAA, EPT>(a, reinterpret_cast<const int32_t*>(smem + lay.meta_off[0] + lay.conn_off),
+                                        sinfo[0][0].w, tid, CT, pre, PE);
+        }
+        for (int it = 0; t < a.n_tiles; ++it, t += G) {
+            const int b = it % 3;
+            if (!Cfg::PRE) {
+                mbar_wait(&meta_full[b], (it / 3) & 1);
+                load_nodes<F, DAA, EPT>(a, reinterpret_cast<const int32_t*>(smem + lay.meta_off[b] + lay.conn_off),
+                                        sinfo[b][0].w, tid, CT, X, U);
             }
-        }
-        mbar_wait(&bar[b], (it >> 1) & 1);
-        const int4 i0 = sinfo[b][0], i1 = sinfo[b][1];
-        const int s0 = i0.x, ns = i0.y, e0 = i1.x, ne = i1.y;
-        // byte offsets of this buffer's arrays inside dynamic shared memory
-        const int conn_b = (int)(lay.buf_off[b] + lay.conn_off);
-        const int codes_b = (int)(lay.buf_off[b] + lay.codes_off) +
-                            (int)(reinterpret_cast<uintptr_t>(a.codes16 + i0.z) & 15);
-        const int cnt_b = (int)(lay.buf_off[b] + lay.cnt_off) + (int)(reinterpret_cast<uintptr_t>(a.slot_cnt + s0) & 15);
-        const int32_t* s_conn = reinterpret_cast<const int32_t*>(smem + conn_b);
-        const uint16_t* s_codes = reinterpret_cast<const uint16_t*>(smem + codes_b);
-        const uint8_t* s_cnt = smem + cnt_b;
-
-        // --- A: local matrices of the tile's elements -> shared-memory stage
-        for (int i = tid; i < ((a.debug & 1) ? 0 : ne); i += TB) {
-            double X[N][3], U[N];
+            const int4 i0 = sinfo[b][0];
+            const int e0 = i0.z, ne = i0.w;
+            if (Cfg::PRE) read_nodes<F, DAA, EPT>(pre, PE, ne, tid, CT, X, U);
+            pc.lap(a.dbg, 0);  // loop overhead / meta wait (no PRE) / prefetched nodes
+            typename E::Geo geo[EPT];
 #pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const int64_t v = s_conn[i * N + j];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) X[j][c] = __ldg(&a.coords[3 * v + c]);
-                U[j] = DAA ? __ldg(&a.coeff[v]) : 0.0;
+            for (int k = 0; k < EPT; ++k) {
+                const int e = tid + k * CT;
+                if (e < ne && !E::template geometry<DAA>(X[k], U[k], geo[k]))
+                    atomicMin(a.err, __ldg(&a.elem_list[__ldg(&a.tile_elems[e0 + e])]));
             }
-            SmemStageSink sink{i, a.maxe, ofsA, ofsAa};
-            if (!E::compute(X, U, sink)) atomicMin(a.err, __ldg(&a.elem_list[__ldg(&a.tile_elems[e0 + i])]));
-        }
-
-        // --- B0: exclusive scan of the slot counts -> s_off (first code of each slot)
-        uint16_t* s_off = reinterpret_cast<uint16_t*>(smem + lay.soff_off);
-        const int chunk = (ns + TB - 1) / TB;
-        const int jb = tid * chunk < ns ? tid * chunk : ns;
-        const int je = jb + chunk < ns ? jb + chunk : ns;
-        int run = 0;
-        for (int j = jb; j < je; ++j) run += s_cnt[j];
-        int incl = run;
+            pc.lap(a.dbg, 1);  // geometry (incl. waiting for the prefetched nodes)
+            if (Cfg::PRE && t + G < a.n_tiles) {  // next tile's nodes -> registers, in flight during the kinds
+                const int bn = (it + 1) % 3;
+                mbar_wait(&meta_full[bn], ((it + 1) / 3) & 1);
+                pc.lap(a.dbg, 2);  // wait for the next tile's metadata
+                prefetch_nodes<F, DAA, EPT>(a, reinterpret_cast<const int32_t*>(smem + lay.meta_off[bn] + lay.conn_off),
+                                            sinfo[bn][0].w, tid, CT, pre, PE);
+            }
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int tv = __shfl_up_sync(0xffffffffu, incl, o);
-            incl += lane >= o ? tv : 0;
-        }
-        if (lane == 31) warp_sums[warp] = incl;
-        __syncthreads();  // stage complete; warp totals visible
-        int wbase = 0;
+            for (int kind = 0; kind < 3; ++kind) {
+                if ((kind == KIND_M && !DM) || (kind == KIND_A && !DA) || (kind == KIND_AA && !DAA)) continue;
+                const int sb = pass & 1;
+                const uint32_t use = pass >> 1;
+                pc.lap(a.dbg, 3);  // prefetch issue / misc
+                if (use > 0) mbar_wait(&stage_empty[sb], (use - 1) & 1);
+                pc.lap(a.dbg, 4);  // wait for a free stage buffer
+                double* st = tile_smem_d + sb * stage_dbl;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) wbase += (w < warp) ? warp_sums[w] : 0;
-        int o2 = wbase + incl - run;
-        for (int j = jb; j < je; ++j) {
-            s_off[j] = (uint16_t)o2;
-            o2 += s_cnt[j];
-        }
-        __syncthreads();
-
-        // --- B1: independent slots, 32 consecutive per warp instruction
-        double* vM = DM ? a.v[0] + s0 : nullptr;
-        double* vA = DA ? a.v[1] + s0 : nullptr;
-        double* vAa = DAA ? a.v[2] + s0 : nullptr;
-        int nh = 0;  // heavy slots recorded by this warp
-        const int jend = (a.debug & 2) ? 0 : ns;
-        for (int j0 = warp * 32; j0 < jend; j0 += TB) {
-            const int j = j0 + lane;
-            const bool in = j < jend;
-            const int c = in ? (int)s_cnt[j] : 0;
-            const int off = in ? (int)s_off[j] : 0;
-            const bool heavy = c > LIGHT;
-            const unsigned hm = __ballot_sync(0xffffffffu, heavy);
-            const int hi = nh + __popc(hm & ((1u << lane) - 1u));
-            nh += __popc(hm);
-            double m = 0.0, st = 0.0, sa = 0.0;
-            if (heavy) {
-                if (hi < MAXH) {
-                    h_list[2 * hi] = j;
-                    h_list[2 * hi + 1] = off;
-                } else {  // list full: sum in place
-                    for (int k = 0; k < c; ++k) {
-                        const int code = s_codes[off + k];
-                        if (DM) m += tile_smem_d[ofsM + code];
-                        if (DA) st += tile_smem_d[ofsA + code];
-                        if (DAA) sa += tile_smem_d[ofsAa + code];
+                for (int k = 0; k < EPT; ++k) {
+                    const int e = tid + k * CT;
+                    if (e < ne && !(a.debug & 1)) {
+                        StageSink sink{st, a.maxe, e};
+                        if (kind == KIND_M) E::template kind<KIND_M>(geo[k], sink);
+                        else if (kind == KIND_A) E::template kind<KIND_A>(geo[k], sink);
+                        else E::template kind<KIND_AA>(geo[k], sink);
                     }
                 }
-            } else if (!(a.debug & 8)) {
+                mbar_arrive(&stage_full[sb]);
+                pc.lap(a.dbg, 5);  // kind contraction + stage stores
+                ++pass;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ reduce warps (+ producer)
+        if (Cfg::REGS_R) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_R));
+        const int rw = warp - CW;
+        uint32_t pass = 0;
+        PhaseClock pc{(a.debug & 4) != 0 && tid == CT, 0};
+        pc.start();
+        for (int it = 0, t = blockIdx.x; t < a.n_tiles; ++it, t += G) {
+            const int b = it % 3;
+            pc.lap(a.dbg, 8);  // misc
+            mbar_wait(&meta_full[b], (it / 3) & 1);
+            pc.lap(a.dbg, 9);  // wait for metadata
+            const int4 i0 = sinfo[b][0], i1 = sinfo[b][1];
+            const int s0 = i0.x, ns = i0.y;
+            const uint32_t* s_pairs =
+                reinterpret_cast<const uint32_t*>(smem + lay.meta_off[b] + lay.pairs_off) + (s0 & 3);
+            const int hw = a.heavy_words, nent = i1.w / hw;
+            const uint16_t* s_heavy =  // entries start 16-B aligned (h0 is a multiple of hw >= 8)
+                reinterpret_cast<const uint16_t*>(smem + lay.meta_off[b] + lay.heavy_off);
 #pragma unroll
-                for (int k = 0; k < LIGHT; ++k) {
-                    const bool take = k < c;
-                    const int code = take ? s_codes[off + k] : 0;
-                    if (DM) m += take ? tile_smem_d[ofsM + code] : 0.0;
-                    if (DA) st += take ? tile_smem_d[ofsA + code] : 0.0;
-                    if (DAA) sa += take ? tile_smem_d[ofsAa + code] : 0.0;
+            for (int kind = 0; kind < 3; ++kind) {
+                if ((kind == KIND_M && !DM) || (kind == KIND_A && !DA) || (kind == KIND_AA && !DAA)) continue;
+                const int sb = pass & 1;
+                pc.lap(a.dbg, 8);
+                mbar_wait(&stage_full[sb], (pass >> 1) & 1);
+                pc.lap(a.dbg, 10);  // wait for a full stage
+                const double* st = tile_smem_d + sb * stage_dbl;
+                double* out = a.v[kind] + s0;
+                const int ns_eff = (a.debug & 2) ? 0 : ns;
+                // light slots (1-2 contributions): UR 32-slot chunks per iteration (independent load chains)
+                constexpr int UR = Cfg::RU;
+                for (int j0 = rw * 32; j0 < ns_eff; j0 += UR * RW * 32) {
+                    uint32_t pw[UR];
+#pragma unroll
+                    for (int u = 0; u < UR; ++u) {
+                        const int j = j0 + u * RW * 32 + lane;
+                        pw[u] = j < ns_eff ? s_pairs[j] : 0xffffffffu;
+                    }
+                    double x0[UR], x1[UR];
+#pragma unroll
+                    for (int u = 0; u < UR; ++u) {
+                        const uint32_t c0 = pw[u] & 0xffffu, c1 = pw[u] >> 16;
+                        x0[u] = c0 != 0xffffu ? st[c0] : 0.0;
+                        x1[u] = c1 != 0xffffu ? st[c1] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < UR; ++u) {
+                        // (0 + x0) + x1: the order of V0 and the oracle; + 0.0 is exact (sums are never -0)
+                        const double v = (0.0 + x0[u]) + x1[u];
+                        if (pw[u] != 0xffffffffu) st_stream(out + j0 + u * RW * 32 + lane, v);
+                    }
                 }
+                pc.lap(a.dbg, 11);  // light slots
+                // heavy slots: one fixed-size entry per lane, loads in parallel, summed in order
+                for (int h = rw * 32 + lane; h < ((a.debug & 2) ? 0 : nent); h += RW * 32) {
+                    const uint4* ent = reinterpret_cast<const uint4*>(s_heavy + h * hw);
+                    const uint4 w0 = ent[0];
+                    const int cnt = (int)(w0.x >> 16);
+                    const uint32_t c[6] = {w0.y & 0xffffu, w0.y >> 16, w0.z & 0xffffu, w0.z >> 16,
+                                           w0.w & 0xffffu, w0.w >> 16};
+                    double x[6];
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) x[k] = c[k] != 0xffffu ? st[c[k]] : 0.0;
+                    double v = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) v = v + x[k];
+                    for (int blk = 1; 6 + 8 * (blk - 1) < cnt; ++blk) {
+                        const uint4 w = ent[blk];
+                        const uint32_t d[8] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16,
+                                               w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
+                        double y[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) y[k] = d[k] != 0xffffu ? st[d[k]] : 0.0;
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) v = v + y[k];
+                    }
+                    st_stream(out + (w0.x & 0xffffu), v);
+                }
+                pc.lap(a.dbg, 12);  // heavy slots
+                mbar_arrive(&stage_empty[sb]);
+                ++pass;
             }
-            if (a.debug & 8) { m = st = sa = (double)c; }
-            if (in && (!heavy || hi >= MAXH) && (!(a.debug & 4) || m == 1.2345e300)) {
-                if (DM) vM[j] = m;
-                if (DA) vA[j] = st;
-                if (DAA) vAa[j] = sa;
+            mbar_arrive(&meta_empty[b]);
+            if (tid == CT && t + 3 * G < a.n_tiles) {
+                pc.lap(a.dbg, 8);
+                mbar_wait(&meta_empty[b], (it / 3) & 1);
+                pc.lap(a.dbg, 13);  // producer: wait for the other reduce warps
+                issue_tile(a, smem, lay, t + 3 * G, b, sinfo, meta_full);
             }
         }
-        __syncwarp();
-        const int nhl = nh < MAXH ? nh : MAXH;
-        for (int h = lane; h < nhl; h += 32) {
-            const int j = h_list[2 * h], off = h_list[2 * h + 1], c = s_cnt[j];
-            double m = 0.0, st = 0.0, sa = 0.0;
-            for (int k = 0; k < c; ++k) {
-                const int code = s_codes[off + k];
-                if (DM) m += tile_smem_d[ofsM + code];
-                if (DA) st += tile_smem_d[ofsA + code];
-                if (DAA) sa += tile_smem_d[ofsAa + code];
-            }
-            if (DM) vM[j] = m;
-            if (DA) vA[j] = st;
-            if (DAA) vAa[j] = sa;
-        }
-        __syncthreads();  // stage and buffer b free for reuse
     }
 }
 
 template <int F>
-size_t tile_smem_bytes(const TilePlan& T, int nk) {
-    return tile_layout(nk, FamInfo<F>::NSYM, FamInfo<F>::NREF, T.max_tile_elems, T.max_tile_codes, T.max_tile_slots,
-                       TileCfg<F>::THREADS / 32, TileCfg<F>::MAXH).total;
+constexpr int tile_capacity() {
+    return TileCfg<F>::CW * 32 * TileCfg<F>::EPT;
 }
 
 template <int F>
-lfem_status ensure_tiles(lfem_plan_s* p, int nk, cudaStream_t s) {
+size_t tile_smem_bytes(const TilePlan& T) {
+    return tile_layout(FamInfo<F>::NSYM, FamInfo<F>::NREF, T.max_tile_elems, T.max_tile_slots, T.max_tile_heavy,
+                       TileCfg<F>::PRE ? tile_capacity<F>() : 0)
+        .total;
+}
+
+// Build the tile plan with an element budget of the compute threads' capacity
+// (or LFEM_TILE_ELEMS), lowered if the 16-bit codes or shared memory do not fit.
+template <int F>
+lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
     TilePlan& T = p->tiles;
-    if (T.ready && T.built_nk >= nk) return LFEM_OK;
-    int R = TileCfg<F>::R;
-    if (const char* env = std::getenv("LFEM_TILE_ROWS")) {
+    if (T.ready) return LFEM_OK;
+    int emax = tile_capacity<F>();
+    if (const char* env = std::getenv("LFEM_TILE_ELEMS")) {
         const int r = std::atoi(env);
-        if (r >= 16) R = r;
+        if (r >= 8 && r < emax) emax = r;
     }
-    if (T.ready && T.rows_per_tile < R) R = T.rows_per_tile;
-    const size_t limit = (size_t)TILE_SMEM_LIMIT / TileCfg<F>::MINB - 2048;
-    for (;;) {
-        LFEM_TRY(build_tiles(p, R, s));
-        if (tile_smem_bytes<F>(T, nk) <= limit && T.max_tile_codes < 65000) break;
-        if (R <= 16) return lfem_fail(LFEM_ERR_UNSUPPORTED, "no row-tile size fits in shared memory");
-        R /= 2;
+    for (int iter = 0;; ++iter) {
+        LFEM_TRY(build_tiles(p, emax, s));
+        if (T.ready && tile_smem_bytes<F>(T) <= (size_t)TILE_SMEM_LIMIT) break;
+        if (emax <= 8 || iter > 16) return lfem_fail(LFEM_ERR_UNSUPPORTED, "no tile size fits the tiled kernel");
+        emax = (int)(emax * 0.9);
     }
-    T.built_nk = nk;
     return LFEM_OK;
 }
 
 template <int F, bool DM, bool DA, bool DAA>
 lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff, double* const vals[3],
                       cudaStream_t s) {
-    constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
-    LFEM_TRY(ensure_tiles<F>(p, NK, s));
+    LFEM_TRY(ensure_tiles<F>(p, s));
     const TilePlan& T = p->tiles;
     if (T.n_tiles == 0) return LFEM_OK;
-    const size_t smem = tile_smem_bytes<F>(T, NK);
+    const size_t smem = tile_smem_bytes<F>(T);
+    constexpr int THREADS = (TileCfg<F>::CW + TileCfg<F>::RW) * 32;
     static int attr_smem = -1;  // per instantiation; one process drives one device
     if (attr_smem < (int)smem) {
         LFEM_CUDA(cudaFuncSetAttribute(k_tiled<F, DM, DA, DAA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
         attr_smem = (int)smem;
     }
-    static int occ = 0;  // resident CTAs per SM for this instantiation
     static int sm_count = 0;
-    if (occ == 0) {
+    if (sm_count == 0) {
         int dev = 0;
         LFEM_CUDA(cudaGetDevice(&dev));
         LFEM_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
-        LFEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<F, DM, DA, DAA>, TileCfg<F>::THREADS,
-                                                                smem));
-        if (occ < 1) occ = 1;
     }
+    int occ = 0;
+    LFEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<F, DM, DA, DAA>, THREADS, smem));
+    if (occ < 1) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tiled kernel does not fit on an SM");
     TileArgs a;
     a.n_tiles = T.n_tiles;
     a.maxe = T.max_tile_elems;
-    a.codes_cap = T.max_tile_codes;
     a.slots_cap = T.max_tile_slots;
+    a.heavy_cap = T.max_tile_heavy;
+    a.heavy_words = T.heavy_words;
     a.tile_info = T.tile_info;
     a.tile_elems = T.tile_elems;
     a.tile_conn = T.tile_conn;
-    a.codes16 = T.codes16;
-    a.slot_cnt = T.slot_cnt;
+    a.pairs = T.pairs;
+    a.heavy = T.heavy;
     a.elem_list = p->elem_list;
     a.coords = coords;
     a.coeff = coeff;
     for (int k = 0; k < 3; ++k) a.v[k] = vals[k];
     a.err = p->err;
     a.debug = 0;
+    a.dbg = nullptr;
     if (const char* env = std::getenv("LFEM_DEBUG_TILED")) a.debug = std::atoi(env);
+    static unsigned long long* dbg = nullptr;
+    if (a.debug & 4) {
+        if (!dbg) LFEM_TRY(dev_alloc_t(&dbg, 16, s));
+        LFEM_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s));
+        a.dbg = dbg;
+    }
     const int grid = T.n_tiles < occ * sm_count ? T.n_tiles : occ * sm_count;
     prof_begin(p, "k_tiled", s);
-    k_tiled<F, DM, DA, DAA><<<grid, TileCfg<F>::THREADS, smem, s>>>(a);
+    k_tiled<F, DM, DA, DAA><<<grid, THREADS, smem, s>>>(a);
     LFEM_CUDA(cudaGetLastError());
     prof_end(p, s);
+    if (a.debug & 4) {  // per-CTA average cycles per phase (one thread per role)
+        unsigned long long h[16];
+        LFEM_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
+        LFEM_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "[tiled phases, kcycles/CTA] grid %d tiles %d R %d maxe %d | compute: misc %.0f geo %.0f "
+                     "meta %.0f pre %.0f wait_stage %.0f kinds %.0f | reduce: misc %.0f meta %.0f wait_stage %.0f "
+                     "light %.0f heavy %.0f producer %.0f\n", grid, T.n_tiles, T.rows_per_tile, T.max_tile_elems,
+                     h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid, h[3] / 1e3 / grid, h[4] / 1e3 / grid,
+                     h[5] / 1e3 / grid, h[8] / 1e3 / grid, h[9] / 1e3 / grid, h[10] / 1e3 / grid, h[11] / 1e3 / grid,
+                     h[12] / 1e3 / grid, h[13] / 1e3 / grid);
+    }
     return LFEM_OK;
 }
 

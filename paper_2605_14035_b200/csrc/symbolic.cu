@@ -175,6 +175,42 @@ inline unsigned grid_for(int64_t n, int threads) {
 
 }  // namespace
 
+// Incidence lists of the owned rows: for row r (plan-relative), inc[inc_ptr[r] ..
+// inc_ptr[r+1]) = the local entries i = e_local * nref + a with conn[e, a] = r,
+// ascending (counting sort by row, then a per-row insertion sort).
+lfem_status build_incidence(lfem_plan_s* p, int64_t** inc_ptr_out, int32_t** inc_out, cudaStream_t s) {
+    const int nref = p->mesh->nref;
+    const int64_t rb = p->row_begin, re = p->row_end, n_rows = re - rb, n_local = p->n_local;
+    int32_t* cnt = nullptr;
+    int64_t* inc_ptr = nullptr;
+    LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
+    LFEM_TRY(dev_alloc_t(&inc_ptr, n_rows + 1, s));
+    LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
+    if (n_local > 0) {
+        k_count<<<grid_for(n_local * nref, 256), 256, 0, s>>>(p->local_conn, n_local, nref, rb, re, cnt);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    LFEM_TRY(scan_exclusive_i32_to_i64(cnt, inc_ptr, n_rows, s));
+    int64_t total_inc = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&total_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    int32_t* inc = nullptr;
+    LFEM_TRY(dev_alloc_t(&inc, total_inc + 1, s));
+    LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
+    if (n_local > 0) {
+        k_fill<<<grid_for(n_local * nref, 256), 256, 0, s>>>(p->local_conn, n_local, nref, rb, re, inc_ptr, cnt, inc);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    if (n_rows > 0) {
+        k_sort_inc<<<grid_for(n_rows, 128), 128, 0, s>>>(inc_ptr, n_rows, inc);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    dev_free(cnt, s);
+    *inc_ptr_out = inc_ptr;
+    *inc_out = inc;
+    return LFEM_OK;
+}
+
 lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     const lfem_mesh_s* m = p->mesh;
     const int nref = m->nref;
@@ -206,33 +242,17 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     dev_free(flag, s);
     dev_free(pos, s);
     // 2. counting sort of local rows by global row
-    int32_t* cnt = nullptr;
     int64_t* inc_ptr = nullptr;
-    LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
-    LFEM_TRY(dev_alloc_t(&inc_ptr, n_rows + 1, s));
-    LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
-    if (n_local > 0) {
-        k_count<<<grid_for(n_local * nref, 256), 256, 0, s>>>(p->local_conn, n_local, nref, rb, re, cnt);
-        LFEM_CUDA(cudaGetLastError());
-    }
-    LFEM_TRY(scan_exclusive_i32_to_i64(cnt, inc_ptr, n_rows, s));
+    int32_t* inc = nullptr;
+    LFEM_TRY(build_incidence(p, &inc_ptr, &inc, s));
     int64_t total_inc = 0;
     LFEM_CUDA(cudaMemcpyAsync(&total_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
     p->n_contrib = total_inc * nref;
     if (p->n_contrib >= (int64_t)INT_MAX)
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "contributions >= 2^31");
-    int32_t* inc = nullptr;
-    LFEM_TRY(dev_alloc_t(&inc, total_inc + 1, s));
-    LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
-    if (n_local > 0) {
-        k_fill<<<grid_for(n_local * nref, 256), 256, 0, s>>>(p->local_conn, n_local, nref, rb, re, inc_ptr, cnt, inc);
-        LFEM_CUDA(cudaGetLastError());
-    }
-    if (n_rows > 0) {
-        k_sort_inc<<<grid_for(n_rows, 128), 128, 0, s>>>(inc_ptr, n_rows, inc);
-        LFEM_CUDA(cudaGetLastError());
-    }
+    int32_t* cnt = nullptr;
+    LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
     // 3. row lengths
     int* overflow = nullptr;
     LFEM_TRY(dev_alloc_t(&overflow, 1, s));
@@ -273,13 +293,10 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
 }
 
 void free_tiles(TilePlan& t, cudaStream_t s) {
-    dev_free(t.tile_elem_ptr, s);
     dev_free(t.tile_elems, s);
-    dev_free(t.tile_conn_ptr, s);
     dev_free(t.tile_conn, s);
     dev_free(t.tile_info, s);
-    dev_free(t.tile_code_ptr, s);
-    dev_free(t.codes16, s);
-    dev_free(t.slot_cnt, s);
+    dev_free(t.pairs, s);
+    dev_free(t.heavy, s);
     t = TilePlan();
 }

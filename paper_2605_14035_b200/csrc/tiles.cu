@@ -1,13 +1,34 @@
 // Row-tile plan of the fused numeric kernel (symbolic phase, one-time).
 //
-// A tile owns R consecutive rows [r0, r1) of the plan, hence the contiguous
+// A tile owns consecutive rows [r0, r1) of the plan, hence the contiguous
 // CSR slot range [row_ptr[r0], row_ptr[r1]).  Its element list holds every
 // plan element with a node in [r0, r1), ascending (halo elements are
 // recomputed by each tile that needs them -- the CTA-level analogue of the
-// multi-GPU row-block partition).  For every slot the
-// contributions keep the symbolic order (ascending element, then (a, b),
-// reading G21) and are re-encoded as 16-bit codes sym(a,b) * maxe + e_tile
-// (the shared-memory stage address), with an 8-bit count per slot.
+// multi-GPU row-block partition).
+//
+// Tile boundaries are chosen by element budget, not by a fixed row count, so
+// that every tile nearly fills the numeric kernel's compute threads.  Greedy,
+// exact: walking the rows in order, a row r adds to the open tile [r0, r) the
+// incident elements that have no owned node in [r0, r), i.e. whose previous
+// owned row prev(e, r) < r0; the tile is closed when the next row would push
+// its element count past the budget.  prev is precomputed per incidence; the
+// walk runs independently on row segments (one thread each, a tile break at
+// every segment start), so it is parallel and deterministic.
+//
+// Reduction codes.  A contribution (e, a, b) of the symbolic plan becomes the
+// 16-bit stage address  code = sym(a,b) * maxe + e_tile  (maxe = max tile
+// elements = stage stride).  Every slot keeps its contributions in symbolic
+// order (ascending element, then (a, b): reading G21) and is described by one
+// 32-bit word:
+//   1 or 2 contributions  (c0, c1)   c1 = 0xffff if there is one
+//   more ("heavy")        0xffffffff
+// so the numeric kernel reads one word per slot and needs no scan.  Heavy
+// slots (vertex diagonals; off-diagonals shared by 3+ elements in bulk) are
+// listed separately per tile as fixed-size entries of HW u16 words
+//   [slot - s0_tile, count, code_0, ..., code_{HW-3}]   (unused codes 0xffff)
+// summed one entry per lane in a second pass; HW = 8, 16, 32, ... is the
+// smallest that holds the mesh's largest slot count (8 = 16 B on icospheres:
+// valence <= 6).
 #include <climits>
 #include <vector>
 
@@ -23,14 +44,13 @@ inline unsigned grid_for(int64_t n, int threads) {
 }
 
 // distinct tiles touched by element le (through its owned rows)
-template <int MAXN>
-__device__ __forceinline__ int elem_tiles(const int32_t* lconn, int nref, int64_t le, int64_t rb, int64_t re, int R,
-                                          int* tiles) {
+__device__ __forceinline__ int elem_tiles(const int32_t* lconn, int nref, int64_t le, int64_t rb, int64_t re,
+                                          const int32_t* __restrict__ tile_of, int* tiles) {
     int nt = 0;
     for (int a = 0; a < nref; ++a) {
         const int64_t r = lconn[le * nref + a];
         if (r < rb || r >= re) continue;
-        const int t = (int)((r - rb) / R);
+        const int t = tile_of[r - rb];
         bool seen = false;
         for (int i = 0; i < nt; ++i) seen |= (tiles[i] == t);
         if (!seen) tiles[nt++] = t;
@@ -38,23 +58,74 @@ __device__ __forceinline__ int elem_tiles(const int32_t* lconn, int nref, int64_
     return nt;
 }
 
+// prev(e, r) for every incidence of the owned rows: the largest owned row of e below r, or -1 (plan-relative)
+__global__ void k_inc_prev(int64_t n_rows, const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc,
+                           const int32_t* __restrict__ lconn, int nref, int64_t rb, int32_t* __restrict__ prev) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t j = inc_ptr[r]; j < inc_ptr[r + 1]; ++j) {
+            const int64_t le = inc[j] / nref;
+            int64_t pv = -1;
+            for (int b = 0; b < nref; ++b) {
+                const int64_t n = (int64_t)lconn[le * nref + b] - rb;
+                if (n >= 0 && n < r && n > pv) pv = n;
+            }
+            prev[j] = (int32_t)pv;
+        }
+    }
+}
+
+// greedy walk over the row segment [seg * seg_rows, ...): start[r] = 1 where a tile opens
+__global__ void k_tile_greedy(int64_t n_rows, int64_t seg_rows, int emax, const int64_t* __restrict__ inc_ptr,
+                              const int32_t* __restrict__ prev, int32_t* __restrict__ start, int* __restrict__ bad) {
+    const int64_t nseg = (n_rows + seg_rows - 1) / seg_rows;
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < nseg; g += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s0 = g * seg_rows, s1 = s0 + seg_rows < n_rows ? s0 + seg_rows : n_rows;
+        int64_t r0 = s0;
+        int cnt = 0;
+        for (int64_t r = s0; r < s1; ++r) {
+            const int64_t j0 = inc_ptr[r], j1 = inc_ptr[r + 1];
+            int nw = 0;
+            for (int64_t j = j0; j < j1; ++j) nw += prev[j] < r0;
+            int st = r == s0;
+            if (r > r0 && cnt + nw > emax) {  // close [r0, r), open a tile at r: all of r's elements are new
+                st = 1;
+                r0 = r;
+                cnt = 0;
+                nw = (int)(j1 - j0);
+            }
+            if (nw > emax) atomicExch(bad, 1);
+            cnt += nw;
+            start[r] = st;
+        }
+    }
+}
+
+__global__ void k_tile_bounds(int64_t n_rows, const int32_t* __restrict__ start, const int64_t* __restrict__ spos,
+                              int64_t* __restrict__ bounds, int32_t* __restrict__ tile_of) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        if (start[r]) bounds[spos[r]] = r;
+        tile_of[r] = (int32_t)(spos[r + 1] - 1);
+        if (r == n_rows - 1) bounds[spos[n_rows]] = n_rows;
+    }
+}
+
 __global__ void k_tile_count(const int32_t* __restrict__ lconn, int64_t n_local, int nref, int64_t rb, int64_t re,
-                             int R, int32_t* __restrict__ cnt) {
+                             const int32_t* __restrict__ tile_of, int32_t* __restrict__ cnt) {
     for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < n_local;
          le += (int64_t)gridDim.x * blockDim.x) {
         int tiles[10];
-        const int nt = elem_tiles<10>(lconn, nref, le, rb, re, R, tiles);
+        const int nt = elem_tiles(lconn, nref, le, rb, re, tile_of, tiles);
         for (int i = 0; i < nt; ++i) atomicAdd(&cnt[tiles[i]], 1);
     }
 }
 
 __global__ void k_tile_fill(const int32_t* __restrict__ lconn, int64_t n_local, int nref, int64_t rb, int64_t re,
-                            int R, const int64_t* __restrict__ ptr, int32_t* __restrict__ cursor,
-                            int32_t* __restrict__ out) {
+                            const int32_t* __restrict__ tile_of, const int64_t* __restrict__ ptr,
+                            int32_t* __restrict__ cursor, int32_t* __restrict__ out) {
     for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < n_local;
          le += (int64_t)gridDim.x * blockDim.x) {
         int tiles[10];
-        const int nt = elem_tiles<10>(lconn, nref, le, rb, re, R, tiles);
+        const int nt = elem_tiles(lconn, nref, le, rb, re, tile_of, tiles);
         for (int i = 0; i < nt; ++i) {
             const int k = atomicAdd(&cursor[tiles[i]], 1);
             out[ptr[tiles[i]] + k] = (int32_t)le;
@@ -86,48 +157,68 @@ __global__ void k_tile_sort(const int64_t* __restrict__ ptr, int n_tiles, const 
     }
 }
 
-// per row: re-encode its contributions; slot counts; tile maxima
-__global__ void k_tile_codes(int64_t n_rows, int R, int nsym, int nref, int64_t n_local, int maxe,
+__global__ void k_max_seg(const int64_t* __restrict__ ptr, int n, int* __restrict__ mx) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
+        atomicMax(mx, (int)(ptr[t + 1] - ptr[t]));
+}
+
+// heavy slots of each row (> 2 contributions) and the largest contribution count
+__global__ void k_row_heavy(int64_t n_rows, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ slot_ptr,
+                            int32_t* __restrict__ nh, int* __restrict__ maxc) {
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
+        int u = 0, m = 0;
+        for (int64_t s = row_ptr[r]; s < row_ptr[r + 1]; ++s) {
+            const int c = slot_ptr[s + 1] - slot_ptr[s];
+            u += c > 2;
+            m = c > m ? c : m;
+        }
+        nh[r] = u;
+        atomicMax(maxc, m);
+    }
+}
+
+// per row: the slot words and heavy entries (see the header)
+__global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of, const int64_t* __restrict__ bounds,
+                             int hw, int64_t n_local, int maxe,
                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ slot_ptr,
                              const int32_t* __restrict__ codes, const int64_t* __restrict__ tptr,
-                             const int32_t* __restrict__ telems, uint16_t* __restrict__ codes16,
-                             uint8_t* __restrict__ slot_cnt, int* __restrict__ bad) {
+                             const int32_t* __restrict__ telems, const int64_t* __restrict__ hptr,
+                             uint32_t* __restrict__ pairs, uint16_t* __restrict__ heavy, int* __restrict__ bad) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
-        const int t = (int)(r / R);
+        const int t = tile_of[r];
         const int32_t* te = telems + tptr[t];
         const int ne = (int)(tptr[t + 1] - tptr[t]);
+        const int64_t sbase = row_ptr[bounds[t]];
+        int64_t cur = hptr[r] * hw;
         for (int64_t s = row_ptr[r]; s < row_ptr[r + 1]; ++s) {
             const int j0 = slot_ptr[s], j1 = slot_ptr[s + 1];
-            if (j1 - j0 > 255) atomicExch(bad, 1);
-            slot_cnt[s] = (uint8_t)(j1 - j0);
+            const int c = j1 - j0;
+            uint32_t code[2] = {0xffffu, 0xffffu};
+            const bool hv = c > 2;
+            if (hv) {
+                if (s - sbase >= 0xffff) atomicExch(bad, 3);
+                pairs[s] = 0xffffffffu;
+                heavy[cur] = (uint16_t)(s - sbase);
+                heavy[cur + 1] = (uint16_t)c;
+                for (int k = c; k < hw - 2; ++k) heavy[cur + 2 + k] = 0xffffu;
+            }
             for (int j = j0; j < j1; ++j) {
-                const int32_t c = codes[j];
-                const int sym = (int)(c / n_local);
-                const int32_t le = (int32_t)(c - (int64_t)sym * n_local);
+                const int32_t cc = codes[j];
+                const int sym = (int)(cc / n_local);
+                const int32_t le = (int32_t)(cc - (int64_t)sym * n_local);
                 int lo = 0, hi = ne;  // lower_bound
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
                     if (te[mid] < le) lo = mid + 1; else hi = mid;
                 }
                 if (lo >= ne || te[lo] != le) atomicExch(bad, 2);
-                codes16[j] = (uint16_t)(sym * maxe + lo);
+                const int64_t v = (int64_t)sym * maxe + lo;
+                if (v >= 0xffff) atomicExch(bad, 4);
+                if (hv) heavy[cur + 2 + (j - j0)] = (uint16_t)v;
+                else code[j - j0] = (uint32_t)v;
             }
-        }
-    }
-}
-
-__global__ void k_tile_sizes(int n_tiles, int R, int64_t n_rows, const int64_t* __restrict__ row_ptr,
-                             const int32_t* __restrict__ slot_ptr, int32_t* __restrict__ code_ptr,
-                             int* __restrict__ maxs, int* __restrict__ maxc) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t <= n_tiles; t += gridDim.x * blockDim.x) {
-        const int64_t r0 = (int64_t)t * R;
-        const int64_t r1 = r0 + R < n_rows ? r0 + R : n_rows;
-        const int64_t s0 = row_ptr[r0 < n_rows ? r0 : n_rows];
-        code_ptr[t] = slot_ptr[s0];
-        if (t < n_tiles) {
-            const int64_t s1 = row_ptr[r1];
-            atomicMax(maxs, (int)(s1 - s0));
-            atomicMax(maxc, (int)(slot_ptr[s1] - slot_ptr[s0]));
+            if (hv) cur += hw;
+            else pairs[s] = code[0] | (code[1] << 16);
         }
     }
 }
@@ -146,53 +237,88 @@ __global__ void k_tile_conn(int n_tiles, int nref, const int64_t* __restrict__ p
     }
 }
 
-// per-tile scalars {s0, ns, c0, nc, e0, ne, q0, nq} (all < 2^31)
-__global__ void k_tile_info(int n_tiles, int R, int64_t n_rows, const int64_t* __restrict__ row_ptr,
-                            const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ eptr,
-                            const int32_t* __restrict__ qptr, int4* __restrict__ info) {
+// per-tile scalars {s0, ns, e0, ne}, {q0, nq, h0, nh} (all < 2^31) and the maxima of ns, nh
+__global__ void k_tile_info(int n_tiles, const int64_t* __restrict__ bounds, int hw, const int64_t* __restrict__ row_ptr,
+                            const int32_t* __restrict__ eptr, const int32_t* __restrict__ qptr,
+                            const int64_t* __restrict__ hptr, int4* __restrict__ info, int* __restrict__ maxs,
+                            int* __restrict__ maxh) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x) {
-        const int64_t r0 = (int64_t)t * R;
-        const int64_t r1 = r0 + R < n_rows ? r0 + R : n_rows;
+        const int64_t r0 = bounds[t], r1 = bounds[t + 1];
         const int64_t s0 = row_ptr[r0], s1 = row_ptr[r1];
-        info[2 * t] = make_int4((int)s0, (int)(s1 - s0), slot_ptr[s0], slot_ptr[s1] - slot_ptr[s0]);
-        info[2 * t + 1] = make_int4(eptr[t], eptr[t + 1] - eptr[t], qptr[t], qptr[t + 1] - qptr[t]);
+        info[2 * t] = make_int4((int)s0, (int)(s1 - s0), eptr[t], eptr[t + 1] - eptr[t]);
+        info[2 * t + 1] = make_int4(qptr[t], qptr[t + 1] - qptr[t], (int)(hptr[r0] * hw), (int)((hptr[r1] - hptr[r0]) * hw));
+        atomicMax(maxs, (int)(s1 - s0));
+        atomicMax(maxh, (int)((hptr[r1] - hptr[r0]) * hw));
     }
-}
-
-__global__ void k_max_seg(const int64_t* __restrict__ ptr, int n, int* __restrict__ mx) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x)
-        atomicMax(mx, (int)(ptr[t + 1] - ptr[t]));
 }
 
 }  // namespace
 
-lfem_status build_tiles(lfem_plan_s* p, int R, cudaStream_t s) {
+lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     free_tiles(p->tiles, s);
     TilePlan& T = p->tiles;
-    const int nref = p->mesh->nref, nsym = p->mesh->nsym;
+    const int nref = p->mesh->nref;
     const int64_t n_rows = p->n_rows, n_local = p->n_local;
-    const int n_tiles = (int)((n_rows + R - 1) / R);
-    T.rows_per_tile = R;
-    T.n_tiles = n_tiles;
-    if (n_tiles == 0) {
+    if (n_rows == 0) {
         T.ready = true;
         return LFEM_OK;
     }
+    // greedy element-budget partition (see the header)
+    int64_t* inc_ptr = nullptr;
+    int32_t* inc = nullptr;
+    LFEM_TRY(build_incidence(p, &inc_ptr, &inc, s));
+    int64_t n_inc = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&n_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    int32_t* prev = nullptr;
+    int32_t* start = nullptr;
+    int64_t* spos = nullptr;
+    int32_t* tile_of = nullptr;
+    int* flags = nullptr;  // [0] overflow/bad, [1] max elems, [2] max slots, [3] max heavy
+    LFEM_TRY(dev_alloc_t(&prev, n_inc + 1, s));
+    LFEM_TRY(dev_alloc_t(&start, n_rows + 1, s));
+    LFEM_TRY(dev_alloc_t(&spos, n_rows + 1, s));
+    LFEM_TRY(dev_alloc_t(&tile_of, n_rows + 1, s));
+    LFEM_TRY(dev_alloc_t(&flags, 4, s));
+    LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
+    k_inc_prev<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, inc_ptr, inc, p->local_conn, nref, p->row_begin, prev);
+    LFEM_CUDA(cudaGetLastError());
+    const int64_t seg_rows = 2048;
+    k_tile_greedy<<<grid_for((n_rows + seg_rows - 1) / seg_rows, 64), 64, 0, s>>>(n_rows, seg_rows, emax, inc_ptr,
+                                                                                  prev, start, flags);
+    LFEM_CUDA(cudaGetLastError());
+    LFEM_TRY(scan_exclusive_i32_to_i64(start, spos, n_rows, s));
+    int64_t nt64 = 0;
+    int hbad = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&nt64, spos + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaMemcpyAsync(&hbad, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    dev_free(inc_ptr, s);
+    dev_free(inc, s);
+    dev_free(prev, s);
+    if (hbad) return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row touches more elements than a tile holds");
+    if (nt64 >= INT_MAX / 2) return lfem_fail(LFEM_ERR_UNSUPPORTED, "too many tiles");
+    const int n_tiles = (int)nt64;
+    int64_t* bounds = nullptr;
     int32_t* cnt = nullptr;
     int64_t* ptr = nullptr;
-    int32_t* tmp = nullptr;
-    int* flags = nullptr;  // [0] overflow/bad, [1] max elems, [2] max slots, [3] max codes
+    LFEM_TRY(dev_alloc_t(&bounds, n_tiles + 1, s));
     LFEM_TRY(dev_alloc_t(&cnt, n_tiles + 1, s));
     LFEM_TRY(dev_alloc_t(&ptr, n_tiles + 1, s));
-    LFEM_TRY(dev_alloc_t(&flags, 4, s));
+    k_tile_bounds<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, start, spos, bounds, tile_of);
+    LFEM_CUDA(cudaGetLastError());
+    dev_free(start, s);
+    dev_free(spos, s);
     LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_tiles + 1), s));
-    LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
     if (n_local > 0) {
         k_tile_count<<<grid_for(n_local, 256), 256, 0, s>>>(p->local_conn, n_local, nref, p->row_begin, p->row_end,
-                                                            R, cnt);
+                                                            tile_of, cnt);
         LFEM_CUDA(cudaGetLastError());
     }
     LFEM_TRY(scan_exclusive_i32_to_i64(cnt, ptr, n_tiles, s));
+    T.n_tiles = n_tiles;
+    T.rows_per_tile = (int)((n_rows + n_tiles - 1) / n_tiles);  // average (reporting only)
+    int32_t* tmp = nullptr;
     int64_t total = 0;
     LFEM_CUDA(cudaMemcpyAsync(&total, ptr + n_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
@@ -200,8 +326,8 @@ lfem_status build_tiles(lfem_plan_s* p, int R, cudaStream_t s) {
     LFEM_TRY(dev_alloc_t(&T.tile_elems, total + 1, s));
     LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_tiles + 1), s));
     if (n_local > 0) {
-        k_tile_fill<<<grid_for(n_local, 256), 256, 0, s>>>(p->local_conn, n_local, nref, p->row_begin, p->row_end, R,
-                                                           ptr, cnt, tmp);
+        k_tile_fill<<<grid_for(n_local, 256), 256, 0, s>>>(p->local_conn, n_local, nref, p->row_begin, p->row_end,
+                                                           tile_of, ptr, cnt, tmp);
         LFEM_CUDA(cudaGetLastError());
     }
     k_tile_sort<<<n_tiles < 148 * 8 ? n_tiles : 148 * 8, 256, 0, s>>>(ptr, n_tiles, tmp, T.tile_elems, flags);
@@ -213,60 +339,87 @@ lfem_status build_tiles(lfem_plan_s* p, int R, cudaStream_t s) {
     LFEM_CUDA(cudaStreamSynchronize(s));
     dev_free(tmp, s);
     if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile element list too long");
-    const int maxe = h[1] > 0 ? h[1] : 1;
-    if ((int64_t)nsym * maxe > 65535) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile too large for 16-bit codes");
+    // stage stride: odd, so the nsym entries of one element fall in different smem banks
+    const int maxe = (h[1] > 0 ? h[1] : 1) | 1;
     T.max_tile_elems = maxe;
-    // element pointers as int32
-    LFEM_TRY(dev_alloc_t(&T.tile_elem_ptr, n_tiles + 1, s));
+    if ((int64_t)p->mesh->nsym * maxe >= 0xffff) {  // 16-bit codes: the caller lowers the budget
+        dev_free(cnt, s);
+        dev_free(ptr, s);
+        dev_free(flags, s);
+        dev_free(bounds, s);
+        dev_free(tile_of, s);
+        return LFEM_OK;
+    }
+    // element / connectivity offsets as int32 (host; n_tiles is small)
+    int32_t* eptr32 = nullptr;
+    int32_t* cptr32 = nullptr;
     {
-        // narrow int64 -> int32 on the host (n_tiles is small)
         std::vector<int64_t> hp(n_tiles + 1);
-        std::vector<int32_t> hp32(n_tiles + 1);
+        std::vector<int32_t> hp32(n_tiles + 1), cp(n_tiles + 1);
         LFEM_CUDA(cudaMemcpy(hp.data(), ptr, sizeof(int64_t) * (n_tiles + 1), cudaMemcpyDeviceToHost));
-        for (int i = 0; i <= n_tiles; ++i) hp32[i] = (int32_t)hp[i];
-        LFEM_CUDA(cudaMemcpy(T.tile_elem_ptr, hp32.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
-        std::vector<int32_t> cp(n_tiles + 1);
         int64_t acc = 0;
-        for (int i = 0; i < n_tiles; ++i) {
+        for (int i = 0; i <= n_tiles; ++i) {
+            hp32[i] = (int32_t)hp[i];
             cp[i] = (int32_t)acc;
-            acc += ((hp[i + 1] - hp[i]) * nref + 3) & ~int64_t(3);
+            if (i < n_tiles) acc += ((hp[i + 1] - hp[i]) * nref + 3) & ~int64_t(3);
         }
-        cp[n_tiles] = (int32_t)acc;
-        if (acc >= INT_MAX) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile connectivity >= 2^31 entries");
-        LFEM_TRY(dev_alloc_t(&T.tile_conn_ptr, n_tiles + 1, s));
+        if (acc >= INT_MAX || hp[n_tiles] >= INT_MAX)
+            return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile connectivity >= 2^31 entries");
+        LFEM_TRY(dev_alloc_t(&eptr32, n_tiles + 1, s));
+        LFEM_TRY(dev_alloc_t(&cptr32, n_tiles + 1, s));
         LFEM_TRY(dev_alloc_t(&T.tile_conn, acc + 16, s));
-        LFEM_CUDA(cudaMemcpy(T.tile_conn_ptr, cp.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
+        LFEM_CUDA(cudaMemcpy(eptr32, hp32.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
+        LFEM_CUDA(cudaMemcpy(cptr32, cp.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
         k_tile_conn<<<n_tiles < 148 * 16 ? n_tiles : 148 * 16, 256, 0, s>>>(n_tiles, nref, ptr, T.tile_elems,
-                                                                          p->local_conn, T.tile_conn_ptr, T.tile_conn);
+                                                                          p->local_conn, cptr32, T.tile_conn);
         LFEM_CUDA(cudaGetLastError());
     }
-    // codes
-    LFEM_TRY(dev_alloc_t(&T.codes16, p->n_contrib + 64, s));  // bulk copies read up to 16 B past the end
-    LFEM_TRY(dev_alloc_t(&T.slot_cnt, p->nnz + 64, s));
-    LFEM_TRY(dev_alloc_t(&T.tile_code_ptr, n_tiles + 1, s));
+    // heavy entries: per-row heavy-slot counts -> global entry offsets; entry size from the largest count
+    int32_t* hu = nullptr;
+    int64_t* hptr = nullptr;
+    LFEM_TRY(dev_alloc_t(&hu, n_rows + 1, s));
+    LFEM_TRY(dev_alloc_t(&hptr, n_rows + 1, s));
+    LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
+    k_row_heavy<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, p->row_ptr, p->slot_ptr, hu, flags + 1);
+    LFEM_CUDA(cudaGetLastError());
+    LFEM_TRY(scan_exclusive_i32_to_i64(hu, hptr, n_rows, s));
+    int64_t heavy_slots = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&heavy_slots, hptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    int hw = 8;
+    while (hw - 2 < h[1]) hw *= 2;
+    if (hw > 256) return lfem_fail(LFEM_ERR_UNSUPPORTED, "a CSR slot has more than 254 contributions");
+    T.heavy_words = hw;
+    if (heavy_slots * hw >= INT_MAX) return lfem_fail(LFEM_ERR_UNSUPPORTED, "heavy lists >= 2^31 entries");
+    // TMA bulk copies round each tile's ranges out to 16 B: pad both arrays
+    LFEM_TRY(dev_alloc_t(&T.pairs, p->nnz + 8, s));
+    LFEM_TRY(dev_alloc_t(&T.heavy, heavy_slots * hw + 16, s));
     LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
     if (n_rows > 0) {
-        k_tile_codes<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, R, nsym, nref, n_local, maxe, p->row_ptr,
-                                                           p->slot_ptr, p->codes, ptr, T.tile_elems, T.codes16,
-                                                           T.slot_cnt, flags);
+        k_tile_pairs<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, tile_of, bounds, hw, n_local, maxe, p->row_ptr,
+                                                           p->slot_ptr,
+                                                           p->codes, ptr, T.tile_elems, hptr, T.pairs, T.heavy, flags);
         LFEM_CUDA(cudaGetLastError());
     }
-    k_tile_sizes<<<grid_for(n_tiles + 1, 256), 256, 0, s>>>(n_tiles, R, n_rows, p->row_ptr, p->slot_ptr,
-                                                            T.tile_code_ptr, flags + 2, flags + 3);
+    LFEM_TRY(dev_alloc_t(&T.tile_info, (size_t)2 * n_tiles + 2, s));
+    k_tile_info<<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, bounds, hw, p->row_ptr, eptr32, cptr32, hptr,
+                                                       T.tile_info, flags + 2, flags + 3);
     LFEM_CUDA(cudaGetLastError());
     LFEM_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
     dev_free(cnt, s);
     dev_free(ptr, s);
     dev_free(flags, s);
-    if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile code construction failed");
-    LFEM_TRY(dev_alloc_t(&T.tile_info, (size_t)2 * n_tiles + 2, s));
-    k_tile_info<<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, R, n_rows, p->row_ptr, p->slot_ptr, T.tile_elem_ptr,
-                                                       T.tile_conn_ptr, T.tile_info);
-    LFEM_CUDA(cudaGetLastError());
-    LFEM_CUDA(cudaStreamSynchronize(s));
+    dev_free(hu, s);
+    dev_free(hptr, s);
+    dev_free(eptr32, s);
+    dev_free(cptr32, s);
+    dev_free(bounds, s);
+    dev_free(tile_of, s);
+    if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile code construction failed (" + std::to_string(h[0]) + ")");
     T.max_tile_slots = h[2];
-    T.max_tile_codes = h[3];
+    T.max_tile_heavy = h[3];
     T.ready = true;
     return LFEM_OK;
 }
