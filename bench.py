@@ -70,20 +70,6 @@ def build_mesh(name):
     return m, time.time() - t0
 
 
-def partition_rows(conn, n_nodes, world):
-    """Contiguous row blocks balanced by incident (element, local row) counts."""
-    if world == 1:
-        return [0, n_nodes]
-    w = np.bincount(conn.ravel(), minlength=n_nodes).astype(np.int64)
-    c = np.cumsum(w)
-    tot = int(c[-1])
-    bounds = [0]
-    for r in range(1, world):
-        bounds.append(int(np.searchsorted(c, tot * r / world)))
-    bounds.append(n_nodes)
-    return bounds
-
-
 class ClockSampler:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -132,16 +118,29 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
+def _oracle_rows_for(m, kinds, coeff, target_s, nt):
+    """Rows of a contiguous block that take about target_s seconds in the oracle:
+    two calibration runs separate the per-call setup from the per-row cost."""
+    import oracle
+    r1 = min(m.n_nodes, 20000)
+    r2 = min(m.n_nodes, 2 * r1)
+    t0 = time.perf_counter()
+    oracle.assemble_rows(m, kinds, rows=np.arange(r1, dtype=np.int64), coeff=coeff, nthreads=nt)
+    t1 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.assemble_rows(m, kinds, rows=np.arange(r2, dtype=np.int64), coeff=coeff, nthreads=nt)
+    t2 = time.perf_counter() - t0
+    per_row = max((t2 - t1) / max(1, r2 - r1), 1e-9)
+    rows = int(r2 + max(0.0, target_s - t2) / per_row)
+    return int(min(m.n_nodes, max(r1, rows)))
+
+
 def oracle_sample(m, kinds, coeff, target_s):
     """Time the oracle as it stands on a contiguous block of rows sized for
     about target_s seconds; returns (elements/s equivalent, rows, seconds, threads)."""
     import oracle
     nt = os.cpu_count() or 1
-    rows0 = min(m.n_nodes, 20000)
-    t0 = time.perf_counter()
-    oracle.assemble_rows(m, kinds, rows=np.arange(rows0, dtype=np.int64), coeff=coeff, nthreads=nt)
-    dt0 = time.perf_counter() - t0
-    rows = int(min(m.n_nodes, max(rows0, rows0 * target_s / max(dt0, 1e-3))))
+    rows = _oracle_rows_for(m, kinds, coeff, target_s, nt)
     t0 = time.perf_counter()
     c = oracle.assemble_rows(m, kinds, rows=np.arange(rows, dtype=np.int64), coeff=coeff, nthreads=nt)
     dt = time.perf_counter() - t0
@@ -161,12 +160,8 @@ def run_reference(args):
     nt = os.cpu_count() or 1
     # calibrate, then size each step for ~budget/(K+W) seconds
     budget = float(os.environ.get("LFEM_REF_BUDGET_S", "90"))
-    rows0 = min(m.n_nodes, 20000)
-    t0 = time.perf_counter()
-    oracle.assemble_rows(m, kinds, rows=np.arange(rows0, dtype=np.int64), coeff=coeff, nthreads=nt)
-    dt0 = time.perf_counter() - t0
     per_step = budget / max(1, args.steps + args.warmup)
-    rows = int(min(m.n_nodes, max(2000, rows0 * per_step / max(dt0, 1e-3))))
+    rows = max(2000, _oracle_rows_for(m, kinds, coeff, per_step, nt))
     times = []
     for it in range(args.warmup + args.steps):
         r0 = (it * rows) % max(1, m.n_nodes - rows + 1)
@@ -197,6 +192,7 @@ def run_lfem(args):
     import torch.distributed as dist
 
     from paper_2605_14035_b200 import lfem
+    from paper_2605_14035_b200.partition import partition_rows
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
