@@ -42,8 +42,10 @@ struct TilePlan {
     int max_tile_heavy = 0;     // max heavy-list u16 words per tile
     int heavy_words = 8;        // u16 words per heavy entry (16-B multiple)
     int32_t* tile_elems = nullptr;      // plan-local element ids, ascending per tile
-    int32_t* tile_conn = nullptr;       // per tile: its elements' connectivity in tile order (16-B padded)
-    int4* tile_info = nullptr;          // 2 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}
+    int max_tile_nodes = 0;     // max owned rows + halo nodes per tile
+    uint16_t* conn16 = nullptr;         // per tile: its elements' tile-local node indices (16-B padded)
+    int32_t* halo = nullptr;            // per tile: halo nodes (global ids, sorted; 16-B padded)
+    int4* tile_info = nullptr;          // 3 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}, {g0, nrows, l0, nl}
     uint32_t* pairs = nullptr;          // nnz: per slot, (c0 | c1 << 16); c1 = 0xffff if one contribution;
                                         // 0xffffffff for a heavy slot (> 2 contributions)
     uint16_t* heavy = nullptr;          // per heavy slot: [slot - s0, count, codes...] (fixed size per family)

@@ -63,6 +63,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// order this thread's (and, after a barrier, the CTA's) generic-proxy shared
+// memory accesses before subsequent async-proxy (TMA) writes to the same buffer
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     uint32_t done = 0;
     do {
@@ -90,40 +94,49 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 
 // CW compute warps, RW reduce warps, EPT elements per compute thread (tile
 // element budget CW*32*EPT), RU light-slot chunks per reduce iteration,
-// REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default),
-// PRE: prefetch the next tile's nodes (cp.async) during the current tile.
+// REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default).
 template <int F> struct TileCfg;
-template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 2, RU = LFEM_RU, REGS_C = 0, REGS_R = 0; static constexpr bool PRE = true; };
-template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_RW == 8 ? 168 : 0, REGS_R = LFEM_RW == 8 ? 88 : 0; static constexpr bool PRE = true; };
-template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; static constexpr bool PRE = false; };
-template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; static constexpr bool PRE = false; };
+template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 2, RU = LFEM_RU, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_RW == 8 ? 168 : 0, REGS_R = LFEM_RW == 8 ? 88 : 0; };
+template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 
 struct TileLayout {
     size_t stage_bytes;           // one stage buffer
-    size_t meta_off[3], conn_off, pairs_off, heavy_off, meta_bytes, pre_off, total;
+    size_t meta_off[3], conn_off, pairs_off, heavy_off, halo_off, meta_bytes;
+    size_t node_off[2], xyz_off, u_off, node_bytes, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
-// stage[2] | meta[3] = {conn | pairs | heavy}
+// stage[2] | meta[3] = {conn16 | pairs | heavy | halo} | nodes[2] = {xyz | u}
 __host__ __device__ inline TileLayout tile_layout(int nsym, int nref, int maxe, int slots_cap, int heavy_cap,
-                                                  int pre_elems) {
+                                                  int nodes_cap) {
     TileLayout L;
     L.stage_bytes = align16(sizeof(double) * (size_t)nsym * maxe);
     L.conn_off = 0;
-    L.pairs_off = align16(sizeof(int32_t) * ((size_t)maxe * nref + 4));
+    L.pairs_off = align16(sizeof(uint16_t) * ((size_t)maxe * nref + 8));
     L.heavy_off = L.pairs_off + align16(sizeof(uint32_t) * ((size_t)slots_cap + 8));
-    L.meta_bytes = L.heavy_off + align16(sizeof(uint16_t) * ((size_t)heavy_cap + 16));
-    for (int b = 0; b < 3; ++b) L.meta_off[b] = 2 * L.stage_bytes + b * L.meta_bytes;
-    L.pre_off = 2 * L.stage_bytes + 3 * L.meta_bytes;
-    L.total = L.pre_off + sizeof(double) * (size_t)4 * nref * pre_elems;  // pre[j][c][e]: x, y, z, u
+    L.halo_off = L.heavy_off + align16(sizeof(uint16_t) * ((size_t)heavy_cap + 16));
+    L.meta_bytes = L.halo_off + align16(sizeof(int32_t) * ((size_t)nodes_cap + 4));
+    L.xyz_off = 0;
+    L.u_off = align16(sizeof(double) * (3 * (size_t)nodes_cap + 2));
+    L.node_bytes = L.u_off + align16(sizeof(double) * ((size_t)nodes_cap + 2));
+    size_t o = 2 * L.stage_bytes;
+    for (int b = 0; b < 3; ++b) L.meta_off[b] = o + b * L.meta_bytes;
+    o += 3 * L.meta_bytes;
+    for (int b = 0; b < 2; ++b) L.node_off[b] = o + b * L.node_bytes;
+    L.total = o + 2 * L.node_bytes;
     return L;
 }
 
 struct TileArgs {
     int n_tiles;
     int maxe, slots_cap, heavy_cap, heavy_words;
-    const int4* tile_info;      // 2 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}
+    int nodes_cap;
+    int64_t n_nodes;
+    const int4* tile_info;      // 3 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}, {g0, nrows, l0, nl}
     const int32_t* tile_elems;
-    const int32_t* tile_conn;
+    const uint16_t* conn16;
+    const int32_t* halo;
     const uint32_t* pairs;
     const uint16_t* heavy;
     const int32_t* elem_list;
@@ -146,18 +159,22 @@ struct StageSink {  // stage[s * maxe + e]
 
 // producer: publish tile t's info in sinfo[b] and start its bulk copies into meta buffer b
 __device__ __forceinline__ void issue_tile(const TileArgs& a, unsigned char* smem, const TileLayout& lay, int t,
-                                           int b, int4 (*sinfo)[2], uint64_t* bar) {
-    const int4 i0 = a.tile_info[2 * t], i1 = a.tile_info[2 * t + 1];
+                                           int b, int4 (*sinfo)[3], uint64_t* bar) {
+    const int4 i0 = a.tile_info[3 * t], i1 = a.tile_info[3 * t + 1], i2 = a.tile_info[3 * t + 2];
     sinfo[b][0] = i0;
     sinfo[b][1] = i1;
+    sinfo[b][2] = i2;
     unsigned char* buf = smem + lay.meta_off[b];
     const int p0 = i0.x & ~3, p1 = (i0.x + i0.y + 3) & ~3;    // u32, 16-B aligned
     const int h0 = i1.z & ~7, h1 = (i1.z + i1.w + 7) & ~7;    // u16, 16-B aligned
-    const uint32_t bq = (uint32_t)i1.y * 4u, bp = (uint32_t)(p1 - p0) * 4u, bh = (uint32_t)(h1 - h0) * 2u;
-    mbar_arrive_expect_tx(&bar[b], bq + bp + bh);
-    if (bq) bulk_g2s(buf + lay.conn_off, a.tile_conn + i1.x, bq, &bar[b]);
+    const uint32_t bq = (uint32_t)i1.y * 2u, bp = (uint32_t)(p1 - p0) * 4u, bh = (uint32_t)(h1 - h0) * 2u;
+    const uint32_t bl = (uint32_t)((i2.w + 3) & ~3) * 4u;     // halo list, 16-B padded per tile
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&bar[b], bq + bp + bh + bl);
+    if (bq) bulk_g2s(buf + lay.conn_off, a.conn16 + i1.x, bq, &bar[b]);
     if (bp) bulk_g2s(buf + lay.pairs_off, a.pairs + p0, bp, &bar[b]);
     if (bh) bulk_g2s(buf + lay.heavy_off, a.heavy + h0, bh, &bar[b]);
+    if (bl) bulk_g2s(buf + lay.halo_off, a.halo + i2.z, bl, &bar[b]);
 }
 
 __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
@@ -166,63 +183,65 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// The thread's elements e = ci + k*ct of a tile: node coordinates (and u) either
-// gathered straight into registers (load_nodes) or prefetched asynchronously
-// into the thread's own slots of pre[j][c][e] (prefetch_nodes, cp.async ->
-// LDGSTS; no registers held while in flight) and read back later (read_nodes).
-template <int F, bool COEF, int EPT>
-__device__ __forceinline__ void load_nodes(const TileArgs& a, const int32_t* s_conn, int ne, int ci, int ct,
-                                           double (&X)[EPT][FamInfo<F>::NREF][3], double (&U)[EPT][FamInfo<F>::NREF]) {
-    constexpr int N = FamInfo<F>::NREF;
-#pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-        const int e = ci + k * ct;
-        if (e < ne) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const int64_t v = s_conn[e * N + j];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) X[k][j][c] = __ldg(&a.coords[3 * v + c]);
-                U[k][j] = COEF ? __ldg(&a.coeff[v]) : 0.0;
-            }
-        }
+// Node buffer of a tile: its owned rows [g0, g0 + nrows) -- one contiguous
+// range of coords (24 B per node) and u (8 B) -- come in by two TMA bulk
+// copies (16-B aligned around the range: o3 / o1 doubles of lead-in), issued
+// by one compute thread on node_full; its halo nodes (sorted global ids in
+// the meta buffer) are gathered by all compute threads with cp.async (LDGSTS).
+// Node l of the tile is at xyz[o3 + 3 l], u[o1 + l]; halo node h is node
+// nrows + 1 + h (the rounded-out bulk copy may write one double past the owned
+// range, so one node slot is left free between the two).
+__device__ __forceinline__ void prefetch_tile_nodes(const TileArgs& a, bool coef, const int4& i2,
+                                                    const int32_t* s_halo, unsigned char* nb, const TileLayout& lay,
+                                                    uint64_t* node_full, int tid, int ct) {
+    double* xyz = reinterpret_cast<double*>(nb + lay.xyz_off);
+    double* u = reinterpret_cast<double*>(nb + lay.u_off);
+    const int64_t g0 = i2.x;
+    const int nrows = i2.y, nh = i2.w;
+    const int64_t x0 = 3 * g0, x0a = x0 & ~int64_t(1), xe = 3 * (g0 + nrows);
+    const int64_t u0a = g0 & ~int64_t(1), ue = g0 + nrows;
+    int64_t x1a = (xe + 1) & ~int64_t(1), u1a = (ue + 1) & ~int64_t(1);
+    if (x1a > 3 * a.n_nodes) x1a -= 2;  // never read past the caller's arrays: the tail goes by cp.async
+    if (u1a > a.n_nodes) u1a -= 2;
+    const int o3 = (int)(x0 - x0a), o1 = (int)(g0 - u0a);
+    if (tid == 0) {
+        const uint32_t bx = x1a > x0a ? (uint32_t)(x1a - x0a) * 8u : 0u;
+        const uint32_t bu = coef && u1a > u0a ? (uint32_t)(u1a - u0a) * 8u : 0u;
+        fence_proxy_async();
+        mbar_arrive_expect_tx(node_full, bx + bu);
+        if (bx) bulk_g2s(xyz, a.coords + x0a, bx, node_full);
+        if (bu) bulk_g2s(u, a.coeff + u0a, bu, node_full);
+        for (int64_t i = x1a > x0a ? x1a : x0a; i < xe; ++i) cp_async8(xyz + (i - x0a), a.coords + i);
+        if (coef)
+            for (int64_t i = u1a > u0a ? u1a : u0a; i < ue; ++i) cp_async8(u + (i - u0a), a.coeff + i);
     }
-}
-
-template <int F, bool COEF, int EPT>
-__device__ __forceinline__ void prefetch_nodes(const TileArgs& a, const int32_t* s_conn, int ne, int ci, int ct,
-                                               double* pre, int pe) {
-    constexpr int N = FamInfo<F>::NREF;
+    for (int h = tid; h < nh; h += ct) {
+        const int64_t v = s_halo[h];
+        const int l = nrows + 1 + h;
 #pragma unroll
-    for (int k = 0; k < EPT; ++k) {
-        const int e = ci + k * ct;
-        if (e < ne) {
-#pragma unroll
-            for (int j = 0; j < N; ++j) {
-                const int64_t v = s_conn[e * N + j];
-#pragma unroll
-                for (int c = 0; c < 3; ++c) cp_async8(pre + (j * 4 + c) * pe + e, a.coords + 3 * v + c);
-                if (COEF) cp_async8(pre + (j * 4 + 3) * pe + e, a.coeff + v);
-            }
-        }
+        for (int c = 0; c < 3; ++c) cp_async8(xyz + o3 + 3 * l + c, a.coords + 3 * v + c);
+        if (coef) cp_async8(u + o1 + l, a.coeff + v);
     }
     cp_async_commit();
 }
 
 template <int F, bool COEF, int EPT>
-__device__ __forceinline__ void read_nodes(const double* pre, int pe, int ne, int ci, int ct,
+__device__ __forceinline__ void read_nodes(const int4& i2, const uint16_t* s_conn, const unsigned char* nb,
+                                           const TileLayout& lay, int ne, int ci, int ct,
                                            double (&X)[EPT][FamInfo<F>::NREF][3], double (&U)[EPT][FamInfo<F>::NREF]) {
     constexpr int N = FamInfo<F>::NREF;
-    cp_async_wait_all();
+    const double* xyz = reinterpret_cast<const double*>(nb + lay.xyz_off) + ((3 * (int64_t)i2.x) & 1);
+    const double* u = reinterpret_cast<const double*>(nb + lay.u_off) + (i2.x & 1);
 #pragma unroll
     for (int k = 0; k < EPT; ++k) {
         const int e = ci + k * ct;
         if (e < ne) {
 #pragma unroll
             for (int j = 0; j < N; ++j) {
+                const int l = s_conn[e * N + j];
 #pragma unroll
-                for (int c = 0; c < 3; ++c) X[k][j][c] = pre[(j * 4 + c) * pe + e];
-                U[k][j] = COEF ? pre[(j * 4 + 3) * pe + e] : 0.0;
+                for (int c = 0; c < 3; ++c) X[k][j][c] = xyz[3 * l + c];
+                U[k][j] = COEF ? u[l] : 0.0;
             }
         }
     }
@@ -234,14 +253,12 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
     using Cfg = TileCfg<F>;
     constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
     unsigned char* smem = reinterpret_cast<unsigned char*>(tile_smem_d);
-    __shared__ __align__(8) uint64_t meta_full[3], meta_empty[3], stage_full[2], stage_empty[2];
-    __shared__ int4 sinfo[3][2];
+    __shared__ __align__(8) uint64_t meta_full[3], meta_empty[3], stage_full[2], stage_empty[2], node_full[2];
+    __shared__ int4 sinfo[3][3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
-    constexpr int PE = Cfg::PRE ? CW * 32 * EPT : 0;  // prefetch slots
-    const TileLayout lay = tile_layout(E::NS, N, a.maxe, a.slots_cap, a.heavy_cap, PE);
-    double* pre = reinterpret_cast<double*>(smem + lay.pre_off);
+    const TileLayout lay = tile_layout(E::NS, N, a.maxe, a.slots_cap, a.heavy_cap, a.nodes_cap);
     const int stage_dbl = (int)(lay.stage_bytes / sizeof(double));
 
     if (tid == 0) {
@@ -252,6 +269,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
         for (int b = 0; b < 2; ++b) {
             mbar_init(&stage_full[b], CT);
             mbar_init(&stage_empty[b], RW * 32);
+            mbar_init(&node_full[b], 1);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -272,21 +290,20 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
         pc.start();
         double X[EPT][N][3], U[EPT][N];
         uint32_t pass = 0;
-        if (Cfg::PRE) {
-            mbar_wait(&meta_full[0], 0);
-            prefetch_nodes<F, DAA, EPT>(a, reinterpret_cast<const int32_t*>(smem + lay.meta_off[0] + lay.conn_off),
-                                        sinfo[0][0].w, tid, CT, pre, PE);
-        }
+        mbar_wait(&meta_full[0], 0);
+        prefetch_tile_nodes(a, DAA, sinfo[0][2],
+                            reinterpret_cast<const int32_t*>(smem + lay.meta_off[0] + lay.halo_off),
+                            smem + lay.node_off[0], lay, &node_full[0], tid, CT);
         for (int it = 0; t < a.n_tiles; ++it, t += G) {
-            const int b = it % 3;
-            if (!Cfg::PRE) {
-                mbar_wait(&meta_full[b], (it / 3) & 1);
-                load_nodes<F, DAA, EPT>(a, reinterpret_cast<const int32_t*>(smem + lay.meta_off[b] + lay.conn_off),
-                                        sinfo[b][0].w, tid, CT, X, U);
-            }
-            const int4 i0 = sinfo[b][0];
+            const int b = it % 3, nb = it & 1;
+            const int4 i0 = sinfo[b][0], i2 = sinfo[b][2];
             const int e0 = i0.z, ne = i0.w;
-            if (Cfg::PRE) read_nodes<F, DAA, EPT>(pre, PE, ne, tid, CT, X, U);
+            // this tile's node buffer: TMA part (mbarrier) + every thread's halo gathers (compute-group barrier)
+            mbar_wait(&node_full[nb], (it >> 1) & 1);
+            cp_async_wait_all();
+            asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
+            read_nodes<F, DAA, EPT>(i2, reinterpret_cast<const uint16_t*>(smem + lay.meta_off[b] + lay.conn_off),
+                                    smem + lay.node_off[nb], lay, ne, tid, CT, X, U);
             pc.lap(a.dbg, 0);  // loop overhead / meta wait (no PRE) / prefetched nodes
             typename E::Geo geo[EPT];
 #pragma unroll
@@ -296,12 +313,13 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
                     atomicMin(a.err, __ldg(&a.elem_list[__ldg(&a.tile_elems[e0 + e])]));
             }
             pc.lap(a.dbg, 1);  // geometry (incl. waiting for the prefetched nodes)
-            if (Cfg::PRE && t + G < a.n_tiles) {  // next tile's nodes -> registers, in flight during the kinds
+            if (t + G < a.n_tiles) {  // next tile's nodes -> the other node buffer, in flight during the kinds
                 const int bn = (it + 1) % 3;
                 mbar_wait(&meta_full[bn], ((it + 1) / 3) & 1);
                 pc.lap(a.dbg, 2);  // wait for the next tile's metadata
-                prefetch_nodes<F, DAA, EPT>(a, reinterpret_cast<const int32_t*>(smem + lay.meta_off[bn] + lay.conn_off),
-                                            sinfo[bn][0].w, tid, CT, pre, PE);
+                prefetch_tile_nodes(a, DAA, sinfo[bn][2],
+                                    reinterpret_cast<const int32_t*>(smem + lay.meta_off[bn] + lay.halo_off),
+                                    smem + lay.node_off[nb ^ 1], lay, &node_full[nb ^ 1], tid, CT);
             }
 #pragma unroll
             for (int kind = 0; kind < 3; ++kind) {
@@ -428,7 +446,7 @@ constexpr int tile_capacity() {
 template <int F>
 size_t tile_smem_bytes(const TilePlan& T) {
     return tile_layout(FamInfo<F>::NSYM, FamInfo<F>::NREF, T.max_tile_elems, T.max_tile_slots, T.max_tile_heavy,
-                       TileCfg<F>::PRE ? tile_capacity<F>() : 0)
+                       T.max_tile_nodes)
         .total;
 }
 
@@ -483,7 +501,10 @@ lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff,
     a.heavy_words = T.heavy_words;
     a.tile_info = T.tile_info;
     a.tile_elems = T.tile_elems;
-    a.tile_conn = T.tile_conn;
+    a.conn16 = T.conn16;
+    a.halo = T.halo;
+    a.nodes_cap = T.max_tile_nodes;
+    a.n_nodes = p->mesh->n_nodes;
     a.pairs = T.pairs;
     a.heavy = T.heavy;
     a.elem_list = p->elem_list;

@@ -294,7 +294,8 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
 
 void free_tiles(TilePlan& t, cudaStream_t s) {
     dev_free(t.tile_elems, s);
-    dev_free(t.tile_conn, s);
+    dev_free(t.conn16, s);
+    dev_free(t.halo, s);
     dev_free(t.tile_info, s);
     dev_free(t.pairs, s);
     dev_free(t.heavy, s);

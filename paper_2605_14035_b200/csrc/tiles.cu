@@ -223,32 +223,119 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
     }
 }
 
-// per-tile copy of the element connectivity, tile order, each tile padded to 16 B
-__global__ void k_tile_conn(int n_tiles, int nref, const int64_t* __restrict__ ptr, const int32_t* __restrict__ telems,
-                            const int32_t* __restrict__ lconn, const int32_t* __restrict__ cptr,
-                            int32_t* __restrict__ tconn) {
+// Per tile: its halo nodes (nodes of its elements outside its rows; sorted,
+// unique, global ids) and the elements' tile-local node indices (u16):
+// owned node n -> n - g0, halo node -> nrows + 1 + its rank in the halo list
+// (one slot gap: the kernel's 16-B-rounded bulk copy of the owned range may
+// write one double past it).
+// One block per tile; candidates bitonic-sorted in shared memory.
+constexpr int NODE_MAX = 2048;
+template <int PASS>
+__global__ void __launch_bounds__(256)
+k_tile_nodes(int n_tiles, int nref, int64_t rb, const int64_t* __restrict__ bounds, const int64_t* __restrict__ ptr,
+             const int32_t* __restrict__ telems, const int32_t* __restrict__ lconn, int32_t* __restrict__ hcnt,
+             const int32_t* __restrict__ lptr, const int32_t* __restrict__ cptr, int32_t* __restrict__ halo,
+             uint16_t* __restrict__ conn16, int* __restrict__ bad) {
+    __shared__ int32_t key[NODE_MAX];
+    __shared__ int wsum[8];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    constexpr int PER = NODE_MAX / 256;
     for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
-        const int64_t b = ptr[t];
-        const int n = (int)(ptr[t + 1] - b) * nref;
-        for (int i = threadIdx.x; i < n; i += blockDim.x) {
-            const int e = i / nref, a = i - e * nref;
-            tconn[cptr[t] + i] = lconn[(int64_t)telems[b + e] * nref + a];
+        const int64_t g0 = rb + bounds[t], g1 = rb + bounds[t + 1];
+        const int64_t e0 = ptr[t];
+        const int ne = (int)(ptr[t + 1] - e0), nc = ne * nref;
+        if (nc > NODE_MAX) {
+            if (tid == 0) atomicExch(bad, 6);
+            continue;
         }
+        for (int i = tid; i < NODE_MAX; i += 256) {
+            int32_t v = INT_MAX;
+            if (i < nc) {
+                const int32_t n = lconn[(int64_t)telems[e0 + i / nref] * nref + i % nref];
+                v = (n >= g0 && n < g1) ? INT_MAX : n;
+            }
+            key[i] = v;
+        }
+        __syncthreads();
+        for (int k = 2; k <= NODE_MAX; k <<= 1)  // bitonic sort, ascending
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = tid; i < NODE_MAX; i += 256) {
+                    const int l = i ^ j;
+                    if (l > i) {
+                        const int32_t a = key[i], b = key[l];
+                        if (((i & k) == 0) ? (a > b) : (a < b)) { key[i] = b; key[l] = a; }
+                    }
+                }
+                __syncthreads();
+            }
+        // unique halo nodes: first occurrence of each value != INT_MAX; block scan of the flags
+        int f[PER], cnt = 0;
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int i = tid * PER + q;
+            f[q] = key[i] != INT_MAX && (i == 0 || key[i] != key[i - 1]);
+            cnt += f[q];
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[warp] = incl;
+        __syncthreads();
+        int base = 0, nh = 0;
+        for (int w = 0; w < 8; ++w) {
+            base += w < warp ? wsum[w] : 0;
+            nh += wsum[w];
+        }
+        int pos = base + incl - cnt;
+        if (PASS == 0) {
+            if (tid == 0) hcnt[t] = nh;
+        } else {
+            // compact the unique values to the front of key (in place is unsafe -> via the halo output)
+            int32_t* out = halo + lptr[t];
+#pragma unroll
+            for (int q = 0; q < PER; ++q)
+                if (f[q]) out[pos++] = key[tid * PER + q];
+            __syncthreads();
+            const int nrows = (int)(g1 - g0);
+            for (int i = tid; i < nc; i += 256) {
+                const int32_t n = lconn[(int64_t)telems[e0 + i / nref] * nref + i % nref];
+                int loc;
+                if (n >= g0 && n < g1) {
+                    loc = (int)(n - g0);
+                } else {
+                    int lo = 0, hi = nh;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (out[mid] < n) lo = mid + 1; else hi = mid;
+                    }
+                    loc = nrows + 1 + lo;
+                }
+                if (loc >= 0xffff) atomicExch(bad, 7);
+                conn16[cptr[t] + i] = (uint16_t)loc;
+            }
+        }
+        __syncthreads();
     }
 }
 
-// per-tile scalars {s0, ns, e0, ne}, {q0, nq, h0, nh} (all < 2^31) and the maxima of ns, nh
-__global__ void k_tile_info(int n_tiles, const int64_t* __restrict__ bounds, int hw, const int64_t* __restrict__ row_ptr,
-                            const int32_t* __restrict__ eptr, const int32_t* __restrict__ qptr,
-                            const int64_t* __restrict__ hptr, int4* __restrict__ info, int* __restrict__ maxs,
-                            int* __restrict__ maxh) {
+// per-tile scalars {s0, ns, e0, ne}, {q0, nq, h0, nh}, {g0, nrows, l0, nl} (all < 2^31) and maxima
+__global__ void k_tile_info(int n_tiles, int64_t rb, const int64_t* __restrict__ bounds, int hw,
+                            const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ eptr,
+                            const int32_t* __restrict__ qptr, const int64_t* __restrict__ hptr,
+                            const int32_t* __restrict__ lptr, const int32_t* __restrict__ hcnt, int4* __restrict__ info,
+                            int* __restrict__ maxs, int* __restrict__ maxh, int* __restrict__ maxn) {
     for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x) {
         const int64_t r0 = bounds[t], r1 = bounds[t + 1];
         const int64_t s0 = row_ptr[r0], s1 = row_ptr[r1];
-        info[2 * t] = make_int4((int)s0, (int)(s1 - s0), eptr[t], eptr[t + 1] - eptr[t]);
-        info[2 * t + 1] = make_int4(qptr[t], qptr[t + 1] - qptr[t], (int)(hptr[r0] * hw), (int)((hptr[r1] - hptr[r0]) * hw));
+        info[3 * t] = make_int4((int)s0, (int)(s1 - s0), eptr[t], eptr[t + 1] - eptr[t]);
+        info[3 * t + 1] = make_int4(qptr[t], qptr[t + 1] - qptr[t], (int)(hptr[r0] * hw), (int)((hptr[r1] - hptr[r0]) * hw));
+        info[3 * t + 2] = make_int4((int)(rb + r0), (int)(r1 - r0), lptr[t], hcnt[t]);
         atomicMax(maxs, (int)(s1 - s0));
         atomicMax(maxh, (int)((hptr[r1] - hptr[r0]) * hw));
+        atomicMax(maxn, (int)(r1 - r0) + 1 + hcnt[t]);
     }
 }
 
@@ -350,29 +437,49 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
         dev_free(tile_of, s);
         return LFEM_OK;
     }
-    // element / connectivity offsets as int32 (host; n_tiles is small)
+    // halo nodes per tile (pass 0: counts)
+    int32_t* hcnt = nullptr;
+    LFEM_TRY(dev_alloc_t(&hcnt, n_tiles + 1, s));
+    const unsigned node_grid = n_tiles < 148 * 8 ? n_tiles : 148 * 8;
+    k_tile_nodes<0><<<node_grid, 256, 0, s>>>(n_tiles, nref, p->row_begin, bounds, ptr, T.tile_elems, p->local_conn,
+                                              hcnt, nullptr, nullptr, nullptr, nullptr, flags);
+    LFEM_CUDA(cudaGetLastError());
+    // element / connectivity / halo offsets as int32 (host; n_tiles is small)
     int32_t* eptr32 = nullptr;
     int32_t* cptr32 = nullptr;
+    int32_t* lptr32 = nullptr;
     {
         std::vector<int64_t> hp(n_tiles + 1);
-        std::vector<int32_t> hp32(n_tiles + 1), cp(n_tiles + 1);
+        std::vector<int32_t> hp32(n_tiles + 1), cp(n_tiles + 1), hc(n_tiles + 1), lp(n_tiles + 1);
         LFEM_CUDA(cudaMemcpy(hp.data(), ptr, sizeof(int64_t) * (n_tiles + 1), cudaMemcpyDeviceToHost));
-        int64_t acc = 0;
+        LFEM_CUDA(cudaMemcpy(hc.data(), hcnt, sizeof(int32_t) * n_tiles, cudaMemcpyDeviceToHost));
+        int64_t acc = 0, lacc = 0;
         for (int i = 0; i <= n_tiles; ++i) {
             hp32[i] = (int32_t)hp[i];
             cp[i] = (int32_t)acc;
-            if (i < n_tiles) acc += ((hp[i + 1] - hp[i]) * nref + 3) & ~int64_t(3);
+            lp[i] = (int32_t)lacc;
+            if (i < n_tiles) {
+                acc += ((hp[i + 1] - hp[i]) * nref + 7) & ~int64_t(7);   // u16, 16-B padded
+                lacc += (hc[i] + 3) & ~3;                                // int32, 16-B padded
+            }
         }
-        if (acc >= INT_MAX || hp[n_tiles] >= INT_MAX)
+        if (acc >= INT_MAX || hp[n_tiles] >= INT_MAX || lacc >= INT_MAX)
             return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile connectivity >= 2^31 entries");
         LFEM_TRY(dev_alloc_t(&eptr32, n_tiles + 1, s));
         LFEM_TRY(dev_alloc_t(&cptr32, n_tiles + 1, s));
-        LFEM_TRY(dev_alloc_t(&T.tile_conn, acc + 16, s));
+        LFEM_TRY(dev_alloc_t(&lptr32, n_tiles + 1, s));
+        LFEM_TRY(dev_alloc_t(&T.conn16, acc + 16, s));
+        LFEM_TRY(dev_alloc_t(&T.halo, lacc + 8, s));
         LFEM_CUDA(cudaMemcpy(eptr32, hp32.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
         LFEM_CUDA(cudaMemcpy(cptr32, cp.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
-        k_tile_conn<<<n_tiles < 148 * 16 ? n_tiles : 148 * 16, 256, 0, s>>>(n_tiles, nref, ptr, T.tile_elems,
-                                                                          p->local_conn, cptr32, T.tile_conn);
+        LFEM_CUDA(cudaMemcpy(lptr32, lp.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
+        k_tile_nodes<1><<<node_grid, 256, 0, s>>>(n_tiles, nref, p->row_begin, bounds, ptr, T.tile_elems,
+                                                  p->local_conn, hcnt, lptr32, cptr32, T.halo, T.conn16, flags);
         LFEM_CUDA(cudaGetLastError());
+        int hb = 0;
+        LFEM_CUDA(cudaMemcpyAsync(&hb, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LFEM_CUDA(cudaStreamSynchronize(s));
+        if (hb) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile node lists do not fit (" + std::to_string(hb) + ")");
     }
     // heavy entries: per-row heavy-slot counts -> global entry offsets; entry size from the largest count
     int32_t* hu = nullptr;
@@ -402,9 +509,10 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
                                                            p->codes, ptr, T.tile_elems, hptr, T.pairs, T.heavy, flags);
         LFEM_CUDA(cudaGetLastError());
     }
-    LFEM_TRY(dev_alloc_t(&T.tile_info, (size_t)2 * n_tiles + 2, s));
-    k_tile_info<<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, bounds, hw, p->row_ptr, eptr32, cptr32, hptr,
-                                                       T.tile_info, flags + 2, flags + 3);
+    LFEM_TRY(dev_alloc_t(&T.tile_info, (size_t)3 * n_tiles + 3, s));
+    k_tile_info<<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, p->row_begin, bounds, hw, p->row_ptr, eptr32, cptr32,
+                                                       hptr, lptr32, hcnt, T.tile_info, flags + 2, flags + 3,
+                                                       flags + 1);
     LFEM_CUDA(cudaGetLastError());
     LFEM_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
@@ -415,11 +523,14 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     dev_free(hptr, s);
     dev_free(eptr32, s);
     dev_free(cptr32, s);
+    dev_free(lptr32, s);
+    dev_free(hcnt, s);
     dev_free(bounds, s);
     dev_free(tile_of, s);
     if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile code construction failed (" + std::to_string(h[0]) + ")");
     T.max_tile_slots = h[2];
     T.max_tile_heavy = h[3];
+    T.max_tile_nodes = h[1];
     T.ready = true;
     return LFEM_OK;
 }
