@@ -32,10 +32,14 @@ namespace {
 // --------------------------------------------------------------------------
 // V0: element kernel -> stage[k][s][le]; slot kernel -> vals
 // --------------------------------------------------------------------------
-struct GlobalStageSink {  // stage[s * n_local + le] of one kind
-    double* stage;
-    int64_t n_local, le;
-    __device__ __forceinline__ void operator()(int s, double v) const { stage[(int64_t)s * n_local + le] = v; }
+// V0 stage, element-major: stage[(le * NS + s) * NK + kr] (kr = rank of the kind among the
+// requested ones), so one contribution's values of all kinds are one vector and the
+// contributions of a CSR row come from a few contiguous element blocks.
+struct GlobalStageSink {
+    double* stage;  // already offset by kr
+    int64_t base;   // le * NS * NK
+    int nk;
+    __device__ __forceinline__ void operator()(int s, double v) const { stage[base + (int64_t)s * nk] = v; }
 };
 
 template <int F, bool DM, bool DA, bool DAA>
@@ -44,7 +48,7 @@ k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __r
           const double* __restrict__ coords, const double* __restrict__ coeff, double* __restrict__ stage,
           int* __restrict__ err) {
     using E = Elem<F>;
-    constexpr int N = E::N, NS = E::NS;
+    constexpr int N = E::N, NS = E::NS, NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
     for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < n_local;
          le += (int64_t)gridDim.x * blockDim.x) {
         double X[N][3], U[N];
@@ -57,39 +61,50 @@ k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __r
         }
         typename E::Geo g;
         if (!E::template geometry<DAA>(X, U, g)) atomicMin(err, __ldg(&elem_list[le]));
-        const int64_t stride = (int64_t)NS * n_local;
+        const int64_t base = le * NS * NK;
+        int kr = 0;
         if (DM) {
-            GlobalStageSink sink{stage, n_local, le};
+            GlobalStageSink sink{stage + kr++, base, NK};
             E::template kind<KIND_M>(g, sink);
         }
         if (DA) {
-            GlobalStageSink sink{stage + stride, n_local, le};
+            GlobalStageSink sink{stage + kr++, base, NK};
             E::template kind<KIND_A>(g, sink);
         }
         if (DAA) {
-            GlobalStageSink sink{stage + 2 * stride, n_local, le};
+            GlobalStageSink sink{stage + kr++, base, NK};
             E::template kind<KIND_AA>(g, sink);
         }
     }
 }
 
+// thread per CSR slot; contributions in plan order (ascending element, then (a, b): G21)
 template <bool DM, bool DA, bool DAA>
 __global__ void __launch_bounds__(256)
 k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ codes,
-              const double* __restrict__ stage, int64_t stride, double* __restrict__ vm, double* __restrict__ va,
+              const double* __restrict__ stage, double* __restrict__ vm, double* __restrict__ va,
               double* __restrict__ vaa) {
+    constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
     for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * blockDim.x) {
         const int j0 = __ldg(&slot_ptr[s]), j1 = __ldg(&slot_ptr[s + 1]);
-        double m = 0.0, a = 0.0, aa = 0.0;
+        double acc[NK];
+#pragma unroll
+        for (int k = 0; k < NK; ++k) acc[k] = 0.0;
         for (int j = j0; j < j1; ++j) {
-            const int64_t c = __ldg(&codes[j]);
-            if (DM) m += __ldg(&stage[c]);
-            if (DA) a += __ldg(&stage[stride + c]);
-            if (DAA) aa += __ldg(&stage[2 * stride + c]);
+            const double* p = stage + (int64_t)__ldg(&codes[j]) * NK;
+            if constexpr (NK == 2) {
+                const double2 w = __ldg(reinterpret_cast<const double2*>(p));
+                acc[0] += w.x;
+                acc[1] += w.y;
+            } else {
+#pragma unroll
+                for (int k = 0; k < NK; ++k) acc[k] += __ldg(p + k);
+            }
         }
-        if (DM) vm[s] = m;
-        if (DA) va[s] = a;
-        if (DAA) vaa[s] = aa;
+        int kr = 0;
+        if (DM) vm[s] = acc[kr++];
+        if (DA) va[s] = acc[kr++];
+        if (DAA) vaa[s] = acc[kr++];
     }
 }
 
@@ -114,7 +129,7 @@ lfem_status run_v0(lfem_plan_s* p, const double* coords, const double* coeff, do
     if (p->nnz > 0) {
         prof_begin(p, "k_slot_reduce", s);
         k_slot_reduce<DM, DA, DAA><<<grid_for(p->nnz, 256, 1 << 20), 256, 0, s>>>(
-            p->nnz, p->slot_ptr, p->codes, p->stage, (int64_t)NS * p->n_local, vals[0], vals[1], vals[2]);
+            p->nnz, p->slot_ptr, p->codes, p->stage, vals[0], vals[1], vals[2]);
         LFEM_CUDA(cudaGetLastError());
         prof_end(p, s);
     }

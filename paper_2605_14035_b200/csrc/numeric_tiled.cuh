@@ -181,6 +181,10 @@ __device__ __forceinline__ void cp_async8(void* dst, const void* src) {
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+// arrive on an mbarrier once all of this thread's prior cp.async copies have landed
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // Node buffer of a tile: its owned rows [g0, g0 + nrows) -- one contiguous
@@ -194,6 +198,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void prefetch_tile_nodes(const TileArgs& a, bool coef, const int4& i2,
                                                     const int32_t* s_halo, unsigned char* nb, const TileLayout& lay,
                                                     uint64_t* node_full, int tid, int ct) {
+    // node_full expects 1 + ct arrivals: thread 0's expect_tx (bulk copies) and every
+    // thread's cp.async arrival (its halo gathers); no CTA barrier needed
     double* xyz = reinterpret_cast<double*>(nb + lay.xyz_off);
     double* u = reinterpret_cast<double*>(nb + lay.u_off);
     const int64_t g0 = i2.x;
@@ -222,7 +228,7 @@ __device__ __forceinline__ void prefetch_tile_nodes(const TileArgs& a, bool coef
         for (int c = 0; c < 3; ++c) cp_async8(xyz + o3 + 3 * l + c, a.coords + 3 * v + c);
         if (coef) cp_async8(u + o1 + l, a.coeff + v);
     }
-    cp_async_commit();
+    cp_async_arrive(node_full);
 }
 
 template <int F, bool COEF, int EPT>
@@ -253,7 +259,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
     using Cfg = TileCfg<F>;
     constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
     unsigned char* smem = reinterpret_cast<unsigned char*>(tile_smem_d);
-    __shared__ __align__(8) uint64_t meta_full[3], meta_empty[3], stage_full[2], stage_empty[2], node_full[2];
+    __shared__ __align__(8) uint64_t meta_full[3], meta_empty[3], stage_full[2], stage_empty[2], node_full[2],
+        node_empty[2];
     __shared__ int4 sinfo[3][3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -269,7 +276,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
         for (int b = 0; b < 2; ++b) {
             mbar_init(&stage_full[b], CT);
             mbar_init(&stage_empty[b], RW * 32);
-            mbar_init(&node_full[b], 1);
+            mbar_init(&node_full[b], 1 + CT);
+            mbar_init(&node_empty[b], CT);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -298,12 +306,11 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
             const int b = it % 3, nb = it & 1;
             const int4 i0 = sinfo[b][0], i2 = sinfo[b][2];
             const int e0 = i0.z, ne = i0.w;
-            // this tile's node buffer: TMA part (mbarrier) + every thread's halo gathers (compute-group barrier)
+            // this tile's node buffer: bulk copies + every thread's halo gathers, one mbarrier
             mbar_wait(&node_full[nb], (it >> 1) & 1);
-            cp_async_wait_all();
-            asm volatile("bar.sync 1, %0;" ::"n"(CT) : "memory");
             read_nodes<F, DAA, EPT>(i2, reinterpret_cast<const uint16_t*>(smem + lay.meta_off[b] + lay.conn_off),
                                     smem + lay.node_off[nb], lay, ne, tid, CT, X, U);
+            mbar_arrive(&node_empty[nb]);
             pc.lap(a.dbg, 0);  // loop overhead / meta wait (no PRE) / prefetched nodes
             typename E::Geo geo[EPT];
 #pragma unroll
@@ -316,34 +323,65 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
             if (t + G < a.n_tiles) {  // next tile's nodes -> the other node buffer, in flight during the kinds
                 const int bn = (it + 1) % 3;
                 mbar_wait(&meta_full[bn], ((it + 1) / 3) & 1);
+                const int fill = (it + 1) >> 1;  // fill index of buffer nb ^ 1: its previous contents must be read
+                if (fill > 0) mbar_wait(&node_empty[nb ^ 1], (fill - 1) & 1);
                 pc.lap(a.dbg, 2);  // wait for the next tile's metadata
                 prefetch_tile_nodes(a, DAA, sinfo[bn][2],
                                     reinterpret_cast<const int32_t*>(smem + lay.meta_off[bn] + lay.halo_off),
                                     smem + lay.node_off[nb ^ 1], lay, &node_full[nb ^ 1], tid, CT);
             }
-#pragma unroll
-            for (int kind = 0; kind < 3; ++kind) {
-                if ((kind == KIND_M && !DM) || (kind == KIND_A && !DA) || (kind == KIND_AA && !DAA)) continue;
-                const int sb = pass & 1;
-                const uint32_t use = pass >> 1;
-                pc.lap(a.dbg, 3);  // prefetch issue / misc
-                if (use > 0) mbar_wait(&stage_empty[sb], (use - 1) & 1);
-                pc.lap(a.dbg, 4);  // wait for a free stage buffer
-                double* st = tile_smem_d + sb * stage_dbl;
+            // one kind per stage pass: wait for a free stage buffer, store, hand it to the reduce warps
+#define LFEM_STAGE_ACQUIRE()                                                   \
+    const int sb_ = pass & 1;                                                  \
+    pc.lap(a.dbg, 3);                                                          \
+    if ((pass >> 1) > 0) mbar_wait(&stage_empty[sb_], ((pass >> 1) - 1) & 1);  \
+    pc.lap(a.dbg, 4);                                                          \
+    double* st = tile_smem_d + sb_ * stage_dbl;                                \
+    const bool do_store = !(a.debug & 1)
+#define LFEM_STAGE_RELEASE()              \
+    mbar_arrive(&stage_full[sb_]);        \
+    pc.lap(a.dbg, 5);                     \
+    ++pass
+            if (DM) {
+                LFEM_STAGE_ACQUIRE();
 #pragma unroll
                 for (int k = 0; k < EPT; ++k) {
                     const int e = tid + k * CT;
-                    if (e < ne && !(a.debug & 1)) {
+                    if (e < ne && do_store) {
                         StageSink sink{st, a.maxe, e};
-                        if (kind == KIND_M) E::template kind<KIND_M>(geo[k], sink);
-                        else if (kind == KIND_A) E::template kind<KIND_A>(geo[k], sink);
-                        else E::template kind<KIND_AA>(geo[k], sink);
+                        E::template kind<KIND_M>(geo[k], sink);
                     }
                 }
-                mbar_arrive(&stage_full[sb]);
-                pc.lap(a.dbg, 5);  // kind contraction + stage stores
-                ++pass;
+                LFEM_STAGE_RELEASE();
             }
+            {
+                if (DA) {
+                    LFEM_STAGE_ACQUIRE();
+#pragma unroll
+                    for (int k = 0; k < EPT; ++k) {
+                        const int e = tid + k * CT;
+                        if (e < ne && do_store) {
+                            StageSink sink{st, a.maxe, e};
+                            E::template kind<KIND_A>(geo[k], sink);
+                        }
+                    }
+                    LFEM_STAGE_RELEASE();
+                }
+                if (DAA) {
+                    LFEM_STAGE_ACQUIRE();
+#pragma unroll
+                    for (int k = 0; k < EPT; ++k) {
+                        const int e = tid + k * CT;
+                        if (e < ne && do_store) {
+                            StageSink sink{st, a.maxe, e};
+                            E::template kind<KIND_AA>(geo[k], sink);
+                        }
+                    }
+                    LFEM_STAGE_RELEASE();
+                }
+            }
+#undef LFEM_STAGE_ACQUIRE
+#undef LFEM_STAGE_RELEASE
         }
     } else {
         // ------------------------------------------------------------ reduce warps (+ producer)

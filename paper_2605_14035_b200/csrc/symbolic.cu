@@ -18,7 +18,7 @@
 //      counting in shared memory -> row length; exclusive scan -> row_ptr.
 //   4. k_row_pattern<1>: col_idx (ascending) and the reduction plan: for
 //      every CSR slot the list of its contributions (e, a, b) in ascending
-//      (e, a, b) order (slot_ptr + codes, code = sym(a,b) * n_local + e_local).
+//      (e, a, b) order (slot_ptr + codes, code = e_local * nsym + sym(a,b)).
 #include <climits>
 #include <vector>
 
@@ -96,7 +96,7 @@ __global__ void k_sort_inc(const int64_t* __restrict__ inc_ptr, int64_t n_rows, 
 template <int PASS>
 __global__ void __launch_bounds__(ROW_WARPS * 32)
 k_row_pattern(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc, int64_t n_rows,
-              const int32_t* __restrict__ lconn, int nref, int64_t n_local, int32_t* __restrict__ row_len,
+              const int32_t* __restrict__ lconn, int nref, int nsym, int32_t* __restrict__ row_len,
               const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx, int32_t* __restrict__ slot_ptr,
               int32_t* __restrict__ codes, int* __restrict__ overflow) {
     __shared__ int32_t s_col[ROW_WARPS][MAX_CAND];
@@ -157,7 +157,7 @@ k_row_pattern(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ i
                 const int32_t le = src / nref;
                 const int a = src - le * nref;
                 const int b = i - (i / nref) * nref;
-                codes[cbase + less + before_eq] = (int32_t)((int64_t)sym_index(nref, a, b) * n_local + le);
+                codes[cbase + less + before_eq] = (int32_t)((int64_t)le * nsym + sym_index(nref, a, b));
             }
         }
         __syncwarp();
@@ -259,7 +259,7 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     LFEM_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(n_rows, ROW_WARPS);
     if (n_rows > 0) {
-        k_row_pattern<0><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, n_local, cnt,
+        k_row_pattern<0><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, m->nsym, cnt,
                                                           nullptr, nullptr, nullptr, nullptr, overflow);
         LFEM_CUDA(cudaGetLastError());
     }
@@ -277,7 +277,7 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     LFEM_TRY(dev_alloc_t(&p->slot_ptr, p->nnz + 1, s));
     LFEM_TRY(dev_alloc_t(&p->codes, p->n_contrib + 1, s));
     if (n_rows > 0) {
-        k_row_pattern<1><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, n_local,
+        k_row_pattern<1><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, m->nsym,
                                                           nullptr, p->row_ptr, p->col_idx, p->slot_ptr, p->codes,
                                                           overflow);
         LFEM_CUDA(cudaGetLastError());

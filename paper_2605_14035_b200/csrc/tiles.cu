@@ -179,7 +179,7 @@ __global__ void k_row_heavy(int64_t n_rows, const int64_t* __restrict__ row_ptr,
 
 // per row: the slot words and heavy entries (see the header)
 __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of, const int64_t* __restrict__ bounds,
-                             int hw, int64_t n_local, int maxe,
+                             int hw, int nsym, int maxe,
                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ slot_ptr,
                              const int32_t* __restrict__ codes, const int64_t* __restrict__ tptr,
                              const int32_t* __restrict__ telems, const int64_t* __restrict__ hptr,
@@ -204,8 +204,8 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
             }
             for (int j = j0; j < j1; ++j) {
                 const int32_t cc = codes[j];
-                const int sym = (int)(cc / n_local);
-                const int32_t le = (int32_t)(cc - (int64_t)sym * n_local);
+                const int32_t le = cc / nsym;
+                const int sym = cc - le * nsym;
                 int lo = 0, hi = ne;  // lower_bound
                 while (lo < hi) {
                     const int mid = (lo + hi) >> 1;
@@ -504,7 +504,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     LFEM_TRY(dev_alloc_t(&T.heavy, heavy_slots * hw + 16, s));
     LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
     if (n_rows > 0) {
-        k_tile_pairs<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, tile_of, bounds, hw, n_local, maxe, p->row_ptr,
+        k_tile_pairs<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, tile_of, bounds, hw, p->mesh->nsym, maxe, p->row_ptr,
                                                            p->slot_ptr,
                                                            p->codes, ptr, T.tile_elems, hptr, T.pairs, T.heavy, flags);
         LFEM_CUDA(cudaGetLastError());
