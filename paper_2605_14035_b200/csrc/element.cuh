@@ -64,6 +64,40 @@ struct Shape {
         for (int n = 0; n < D; ++n) z = z && SB(j, m, n) == 0;
         return z;
     }
+    // coefficient of the monomial al (1, x, y, x^2, xy, y^2) in d_m phi_a * d_n phi_b
+    __host__ __device__ static constexpr int TERM(int a, int b, int m, int n, int al) {
+        return al == 0 ? SA(a, m) * SA(b, n)
+             : al == 1 ? SA(a, m) * SB(b, n, 0) + SB(a, m, 0) * SA(b, n)
+             : al == 2 ? SA(a, m) * SB(b, n, 1 % D) + SB(a, m, 1 % D) * SA(b, n)
+             : al == 3 ? SB(a, m, 0) * SB(b, n, 0)
+             : al == 4 ? SB(a, m, 0) * SB(b, n, 1 % D) + SB(a, m, 1 % D) * SB(b, n, 0)
+                       : SB(a, m, 1 % D) * SB(b, n, 1 % D);
+    }
+    // surface: integer coefficient of moment (c, al) in A_loc(a, b), c = 11, 12 (+21), 22
+    __host__ __device__ static constexpr int MCOEF(int a, int b, int c, int al) {
+        return c == 0 ? TERM(a, b, 0, 0, al) : c == 2 ? TERM(a, b, 1 % D, 1 % D, al)
+                                                      : TERM(a, b, 0, 1 % D, al) + TERM(a, b, 1 % D, 0, al);
+    }
+    // compile-time table of MCOEF by symmetric index s = sym(a, b), and which moments are used
+    struct MTab {
+        int k[N * (N + 1) / 2][3][6];
+        bool used[3][6];
+    };
+    __host__ __device__ static constexpr MTab mtab() {
+        MTab t{};
+        for (int c = 0; c < 3; ++c)
+            for (int al = 0; al < 6; ++al) t.used[c][al] = false;
+        for (int a = 0; a < N; ++a)
+            for (int b = a; b < N; ++b) {
+                const int s = b >= a ? a * N - a * (a - 1) / 2 + (b - a) : 0;
+                for (int c = 0; c < 3; ++c)
+                    for (int al = 0; al < 6; ++al) {
+                        t.k[s][c][al] = MCOEF(a, b, c, al);
+                        t.used[c][al] = t.used[c][al] || t.k[s][c][al] != 0;
+                    }
+            }
+        return t;
+    }
     // surface metric-form product gg[s][c] (c: 11, 12+21, 22) vanishes identically
     __host__ __device__ static constexpr bool GGZ(int a, int b, int c) {
         return c == 0 ? (DZ(a, 0) || DZ(b, 0))
@@ -258,29 +292,48 @@ struct Elem {
     static __device__ __forceinline__ void stiffness(const Geo& g, Sink& sink) {
         const RefTab<F>& T = tab<F>();
         if constexpr (D == 2) {
-            double c11[NQ], c12[NQ], c22[NQ];
+            // Moment form.  The reference gradients are affine in xi, so
+            //   A_loc(a,b) = sum_q sum_c K_q^c (d phi_a d phi_b)_c(xi_q)
+            //              = sum_{c, al} MCOEF(a,b,c,al) * mom[c][al],
+            //   mom[c][al] = sum_q K_q^c xi_q^al  (al over 1, x, y, x^2, xy, y^2),
+            // with small integer MCOEF known at compile time (instruction
+            // immediates): 18 moments from 36 table constants instead of one
+            // table constant per term.  Same integrand and rule; only the
+            // rounding order differs from the per-point form (reading G23).
+            constexpr typename S::MTab MT = S::mtab();
+            double mom[3][6];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int al = 0; al < 6; ++al) mom[c][al] = 0.0;
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
-                c11[q] = COEF ? g.aq[q] * g.k11[D == 2 ? q : 0] : g.k11[D == 2 ? q : 0];
-                c12[q] = COEF ? g.aq[q] * g.k12[D == 2 ? q : 0] : g.k12[D == 2 ? q : 0];
-                c22[q] = COEF ? g.aq[q] * g.k22[D == 2 ? q : 0] : g.k22[D == 2 ? q : 0];
+                double kc[3] = {g.k11[D == 2 ? q : 0], g.k12[D == 2 ? q : 0], g.k22[D == 2 ? q : 0]};
+                if (COEF)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) kc[c] = g.aq[q] * kc[c];
+#pragma unroll
+                for (int c = 0; c < 3; ++c)
+#pragma unroll
+                    for (int al = 0; al < 6; ++al)
+                        if (MT.used[c][al]) mom[c][al] = fma(kc[c], T.mono[q][al], mom[c][al]);
             }
-            double v[NS];
 #pragma unroll
-            for (int s = 0; s < NS; ++s) v[s] = 0.0;
+            for (int s = 0; s < NS; ++s) {
+                double v = 0.0;
+                bool first = true;
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
+                for (int c = 0; c < 3; ++c)
 #pragma unroll
-                for (int a = 0; a < N; ++a)
-#pragma unroll
-                    for (int b = a; b < N; ++b) {
-                        const int s = sym_index(N, a, b);
-                        if (!S::GGZ(a, b, 0)) v[s] = fma(c11[q], T.gg[q][s][0], v[s]);
-                        if (!S::GGZ(a, b, 1)) v[s] = fma(c12[q], T.gg[q][s][1], v[s]);
-                        if (!S::GGZ(a, b, 2)) v[s] = fma(c22[q], T.gg[q][s][2], v[s]);
+                    for (int al = 0; al < 6; ++al) {
+                        const int k = MT.k[s][c][al];
+                        if (k != 0) {
+                            v = first ? (double)k * mom[c][al] : fma((double)k, mom[c][al], v);
+                            first = false;
+                        }
                     }
-#pragma unroll
-            for (int s = 0; s < NS; ++s) sink(s, v[s]);
+                sink(s, v);
+            }
         } else {
             double acc[NS];
 #pragma unroll

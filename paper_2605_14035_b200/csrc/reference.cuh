@@ -14,6 +14,7 @@
 //   gg[q][s][0..2] = d1a d1b, d1a d2b + d2a d1b, d2a d2b
 //                  (surface metric form of Eq. Aloc-precise P:337:
 //                   grad_a . C C^T grad_b = d_a^T G^{-1} d_b)
+//   mono[q][0..5] = 1, x, y, x^2, xy, y^2 at xi_q = (x, y) (surface stiffness moments)
 #pragma once
 #include <cmath>
 
@@ -28,6 +29,7 @@ struct RefTab {
     double dphi[NQ][NREF][D];
     double pp[NQ][NSYM];
     double gg[NQ][NSYM][3];
+    double mono[NQ][6];  // 1, x, y, x^2, x y, y^2 at xi_q (surface stiffness moments)
 };
 
 __constant__ RefTab<FAM_TRI_P1> c_tab_tri1;
@@ -142,6 +144,13 @@ void fill(RefTab<F>& t, const Rule& r, int d, int order) {
     for (int q = 0; q < RefTab<F>::NQ; ++q) {
         double phi[10], dphi[10][3];
         basis_eval(d, order, r.xi[q], phi, dphi);
+        const double x = r.xi[q][0], y = r.xi[q][1];
+        t.mono[q][0] = 1.0;
+        t.mono[q][1] = x;
+        t.mono[q][2] = y;
+        t.mono[q][3] = x * x;
+        t.mono[q][4] = x * y;
+        t.mono[q][5] = y * y;
         t.w[q] = r.w[q];
         for (int a = 0; a < N; ++a) {
             t.phi[q][a] = phi[a];
