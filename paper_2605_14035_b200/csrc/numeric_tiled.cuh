@@ -68,6 +68,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    // (a suspend-time hint on try_wait delays the wake-up: measured slower)
     uint32_t done = 0;
     do {
         asm volatile(
@@ -259,7 +260,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
     using Cfg = TileCfg<F>;
     constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
     unsigned char* smem = reinterpret_cast<unsigned char*>(tile_smem_d);
-    __shared__ __align__(8) uint64_t meta_full[3], meta_empty[3], stage_full[2], stage_empty[2], node_full[2],
+    __shared__ int meta_done[3];  // reduce warps done with the tile in meta buffer b
+    __shared__ __align__(8) uint64_t meta_full[3], stage_full[2], stage_empty[2], node_full[2],
         node_empty[2];
     __shared__ int4 sinfo[3][3];
 
@@ -271,7 +273,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
     if (tid == 0) {
         for (int b = 0; b < 3; ++b) {
             mbar_init(&meta_full[b], 1);
-            mbar_init(&meta_empty[b], RW * 32);
+            meta_done[b] = 0;
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&stage_full[b], CT);
@@ -465,12 +467,18 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_t
                 mbar_arrive(&stage_empty[sb]);
                 ++pass;
             }
-            mbar_arrive(&meta_empty[b]);
-            if (tid == CT && t + 3 * G < a.n_tiles) {
-                pc.lap(a.dbg, 8);
-                mbar_wait(&meta_empty[b], (it / 3) & 1);
-                pc.lap(a.dbg, 13);  // producer: wait for the other reduce warps
-                issue_tile(a, smem, lay, t + 3 * G, b, sinfo, meta_full);
+            // the last reduce warp to finish this tile refills meta buffer b (no warp blocks on it)
+            __syncwarp();
+            if (lane == 0) {
+                __threadfence_block();
+                const int done = atomicAdd(&meta_done[b], 1);
+                if (done == RW - 1) {
+                    meta_done[b] = 0;
+                    __threadfence_block();
+                    pc.lap(a.dbg, 8);
+                    if (t + 3 * G < a.n_tiles) issue_tile(a, smem, lay, t + 3 * G, b, sinfo, meta_full);
+                    pc.lap(a.dbg, 13);  // producer
+                }
             }
         }
     }
