@@ -156,7 +156,11 @@ struct Elem {
     // Per-element scalars handed from geometry() to the kind contractions.
     //  surface: w mu, K = (w / mu) adj(G) (3 entries) and a(u_h) per point;
     //  bulk:    w mu and a(u_h) per point + the Jacobian parts J0, J1.
+    // P1 surface: J is constant per element, so the geometry is det*r = mu and
+    // r adj(G) (r = 1/mu), the quadrature weights are applied on the fly.
+    static constexpr bool P1S = (D == 2 && N == 3);
     struct Geo {
+        double mu1, ka[3];  // P1 surface only
         double wmu[NQ];
         double k11[D == 2 ? NQ : 1], k12[D == 2 ? NQ : 1], k22[D == 2 ? NQ : 1];
         double aq[NQ];
@@ -228,6 +232,30 @@ struct Elem {
         double J0[3][D], J1[3][D][D];
         jac_parts(X, J0, J1);
         bool ok = true;
+        if constexpr (P1S) {
+            double J[3][D];
+            jac_at(J0, J1, 0, J);
+            const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+            const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
+            const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
+            const double det = g11 * g22 - g12 * g12;
+            ok = (det > 0.0) & (det < INFINITY);
+            const double r = rsqrt_nr(det);
+            g.mu1 = det * r;
+            g.ka[0] = r * g22;
+            g.ka[1] = -r * g12;
+            g.ka[2] = r * g11;
+            if (COEF) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    double u = 0.0;
+#pragma unroll
+                    for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
+                    g.aq[q] = fma(u, u, 1.0);
+                }
+            }
+            return ok;
+        }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             double J[3][D];
@@ -280,9 +308,11 @@ struct Elem {
 #pragma unroll
         for (int s = 0; s < NS; ++s) m[s] = 0.0;
 #pragma unroll
-        for (int q = 0; q < NQ; ++q)
+        for (int q = 0; q < NQ; ++q) {
+            const double wmu = P1S ? T.w[q] * g.mu1 : g.wmu[q];
 #pragma unroll
-            for (int s = 0; s < NS; ++s) m[s] = fma(g.wmu[q], T.pp[q][s], m[s]);
+            for (int s = 0; s < NS; ++s) m[s] = fma(wmu, T.pp[q][s], m[s]);
+        }
 #pragma unroll
         for (int s = 0; s < NS; ++s) sink(s, m[s]);
     }
@@ -309,6 +339,9 @@ struct Elem {
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 double kc[3] = {g.k11[D == 2 ? q : 0], g.k12[D == 2 ? q : 0], g.k22[D == 2 ? q : 0]};
+                if (P1S)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) kc[c] = T.w[q] * g.ka[c];
                 if (COEF)
 #pragma unroll
                     for (int c = 0; c < 3; ++c) kc[c] = g.aq[q] * kc[c];

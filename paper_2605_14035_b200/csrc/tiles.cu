@@ -229,7 +229,7 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
 // (one slot gap: the kernel's 16-B-rounded bulk copy of the owned range may
 // write one double past it).
 // One block per tile; candidates bitonic-sorted in shared memory.
-constexpr int NODE_MAX = 2048;
+constexpr int NODE_MAX = 4096;  // element-node candidates per tile (P1 triangles: 1024 x 3)
 template <int PASS>
 __global__ void __launch_bounds__(256)
 k_tile_nodes(int n_tiles, int nref, int64_t rb, const int64_t* __restrict__ bounds, const int64_t* __restrict__ ptr,
