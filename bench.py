@@ -333,18 +333,26 @@ def run_lfem(args):
     e2e = None
     if not args.no_e2e:
         coords_h = coords.cpu().pin_memory()
-        coeff_h = coeff.cpu().pin_memory() if coeff is not None else None
         vals_h = [torch.empty(plan.nnz, dtype=torch.float64, pin_memory=True) if vals[i] is not None else None
                   for i in range(3)]
         ke = max(1, min(args.steps, args.e2e_steps))
-        lfem.lfem_assemble_numeric_host(plan, kmask, coords_h, coeff_h, vals_h)
+        # per-step coefficient on the host (C3: u(t), reading G12; else the config's u), pinned, copied in the timed region
+        if coeff is None:
+            coeffs_h = [None] * ke
+        elif u_work is not None:
+            uA, uB = coeff.cpu(), extra_uB.cpu()
+            coeffs_h = [(math.cos(2 * math.pi * (t % 100) / 100) * uA + math.sin(2 * math.pi * (t % 100) / 100) * uB)
+                        .pin_memory() for t in range(ke)]
+        else:
+            coeffs_h = [coeff.cpu().pin_memory()] * ke
+        lfem.lfem_assemble_numeric_host(plan, kmask, coords_h, coeffs_h[0], vals_h)
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for t in range(ke):
-            lfem.lfem_assemble_numeric_host(plan, kmask, coords_h, coeff_h, vals_h)
+            lfem.lfem_assemble_numeric_host(plan, kmask, coords_h, coeffs_h[t], vals_h)
         e1.record(stream)
         torch.cuda.synchronize()
         te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
@@ -354,11 +362,14 @@ def run_lfem(args):
         e2e = {"value": n_elems * ke / (float(te) * 1e-3), "unit": "elements/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(nnz_total * 8 * len(kinds)),
                "api": "lfem_assemble_numeric_host", "steps": ke}
-        # e2e must produce the same bits as the device path
+        # e2e must produce the same bits as the device path with the same inputs
+        cf_last = coeffs_h[-1].to(dev) if coeffs_h[-1] is not None else None
+        lfem.lfem_assemble_numeric(plan, kmask, cf_last, vals)
+        torch.cuda.synchronize()
         for i in range(3):
             if vals[i] is not None:
                 assert torch.equal(vals_h[i], vals[i].cpu()), "e2e values differ from the device path"
-        del vals_h, coords_h, coeff_h
+        del vals_h, coords_h, coeffs_h
 
     # ---- multi-GPU verification: NCCL all_gather of x + local SpMV; checksums all-reduced
     verify = None

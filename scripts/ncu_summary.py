@@ -9,7 +9,9 @@ rep, lcsv, outdir, cfg = sys.argv[1:5]
 os.makedirs(outdir, exist_ok=True)
 raw = subprocess.run(['ncu', '-i', rep, '--page', 'raw', '--csv'], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
-h, v = rows[0], rows[2]
+h = rows[0]
+KSEL = os.environ.get('NCU_KERNEL_ROW')  # which launch of a multi-kernel report (0-based)
+v = rows[2 + int(KSEL)] if KSEL else rows[2]
 m = dict(zip(h, v))
 keys = ['Kernel Name', 'gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
         'dram__throughput.avg.pct_of_peak_sustained_elapsed', 'sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
@@ -55,7 +57,9 @@ if lcsv != '-' and os.path.exists(lcsv):
     t = sum(x[1] for x in acc.values()) or 1
     launches = [f"{x[0]:5d} launches {x[1]/1e3:11.1f} us total {x[1]/max(1,x[0])/1e3:10.1f} us/launch {x[1]/t*100:5.1f}%  {k[:100]}"
                 for k, x in sorted(acc.items(), key=lambda kv: -kv[1][1])]
-with open(os.path.join(outdir, f'ncu_{cfg}_summary.txt'), 'w') as o:
+kshort = m['Kernel Name'].split('(')[0].split('::')[-1].split('<')[0]
+suffix = f"_{kshort}" if KSEL else ""
+with open(os.path.join(outdir, f'ncu_{cfg}{suffix}_summary.txt'), 'w') as o:
     o.write(f"ncu --set full --clock-control none, one launch ({rep})\n\n")
     for k, (x, u) in summ.items(): o.write(f"{k:70s} {x} {u or ''}\n")
     o.write(f"\nDRAM traffic per launch (read + write): {traffic/1e9:.3f} GB\n\nstall reasons (warps per issue):\n")
@@ -66,7 +70,7 @@ with open(os.path.join(outdir, f'ncu_{cfg}_summary.txt'), 'w') as o:
         o.write("\n".join(launches) + "\n")
 tp = os.path.join(os.path.dirname(outdir.rstrip('/')), 'ncu_traffic.json')
 tj = json.load(open(tp)) if os.path.exists(tp) else {}
-kn = 'k_tiled' if 'k_tiled' in summ['Kernel Name'][0] else summ['Kernel Name'][0].split('(')[0].split('::')[-1]
+kn = kshort
 tj[f"{cfg}:{kn}"] = traffic
 json.dump(tj, open(tp, 'w'), indent=1, sort_keys=True)
-print(open(os.path.join(outdir, f'ncu_{cfg}_summary.txt')).read()[:3000])
+print(open(os.path.join(outdir, f'ncu_{cfg}{suffix}_summary.txt')).read()[:1500])
