@@ -37,7 +37,8 @@ struct lfem_mesh_s {
 struct TilePlan {
     int n_tiles = 0;
     int rows_per_tile = 0;      // average rows per tile (tiles are built by element budget)
-    int max_tile_elems = 0;     // max elements per tile = stage stride (codes are sym * maxe + e_tile)
+    int max_tile_elems = 0;     // stage stride: max elements per tile, rounded up to odd (codes are sym * maxe + e_tile)
+    int max_tile_count = 0;     // max elements per tile
     int max_tile_slots = 0;     // max CSR slots per tile
     int max_tile_heavy = 0;     // max heavy-list u16 words per tile
     int heavy_words = 8;        // u16 words per heavy entry (16-B multiple)

@@ -512,6 +512,8 @@ lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
     }
     for (int iter = 0;; ++iter) {
         LFEM_TRY(build_tiles(p, emax, s));
+        if (T.ready && T.max_tile_count > tile_capacity<F>())
+            return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row touches more elements than the tiled kernel's tile holds");
         if (T.ready && tile_smem_bytes<F>(T) <= (size_t)TILE_SMEM_LIMIT) break;
         if (emax <= 8 || iter > 16) return lfem_fail(LFEM_ERR_UNSUPPORTED, "no tile size fits the tiled kernel");
         emax = (int)(emax * 0.9);

@@ -370,6 +370,15 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
     k_inc_prev<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, inc_ptr, inc, p->local_conn, nref, p->row_begin, prev);
     LFEM_CUDA(cudaGetLastError());
+    {  // a tile holds at least one row: the budget is at least the largest row incidence
+        k_max_seg<<<grid_for(n_rows, 256), 256, 0, s>>>(inc_ptr, (int)n_rows, flags + 1);
+        LFEM_CUDA(cudaGetLastError());
+        int maxinc = 0;
+        LFEM_CUDA(cudaMemcpyAsync(&maxinc, flags + 1, sizeof(int), cudaMemcpyDeviceToHost, s));
+        LFEM_CUDA(cudaStreamSynchronize(s));
+        LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
+        if (maxinc > emax) emax = maxinc;
+    }
     const int64_t seg_rows = 2048;
     k_tile_greedy<<<grid_for((n_rows + seg_rows - 1) / seg_rows, 64), 64, 0, s>>>(n_rows, seg_rows, emax, inc_ptr,
                                                                                   prev, start, flags);
@@ -429,6 +438,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     // stage stride: odd, so the nsym entries of one element fall in different smem banks
     const int maxe = (h[1] > 0 ? h[1] : 1) | 1;
     T.max_tile_elems = maxe;
+    T.max_tile_count = h[1];
     if ((int64_t)p->mesh->nsym * maxe >= 0xffff) {  // 16-bit codes: the caller lowers the budget
         dev_free(cnt, s);
         dev_free(ptr, s);

@@ -195,3 +195,50 @@ def test_argument_errors():
     with pytest.raises(lfem.LfemError) as ei:
         lfem.lfem_assemble_symbolic(mh, 5, 2)
     assert ei.value.status == 1
+
+
+# ---------------------------------------------------------------------------- tile-plan edge cases
+@pytest.mark.parametrize("budget", [8, 17, 64, 100])
+@pytest.mark.parametrize("name,mk", [("P2tri", lambda: li.make_config("C5", level_override=3)),
+                                     ("P1tri", lambda: li.make_config("C3", level_override=4)),
+                                     ("P2tet", lambda: li.make_config("C4", level_override=3))],
+                         ids=["P2tri", "P1tri", "P2tet"])
+def test_tiled_small_budgets_bitwise(name, mk, budget, monkeypatch):
+    """Tiny tile element budgets (LFEM_TILE_ELEMS): thousands of tiles with a
+    handful of rows each, single-row tiles, halo-dominated tiles, ragged
+    tails.  Values must be bitwise those of the default plan (summation
+    order is the symbolic order, independent of tiling) and the oracle's
+    within the gate."""
+    m = mk()
+    u = m.coeff if m.coeff is not None else li.random_field(m, 5)
+    kinds = ("M", "A", "Aa")
+    _, rp0, ci0, v0 = gpu_assemble(m, kinds, coeff=u, variant=lfem.LFEM_NUMERIC_V0)
+    monkeypatch.setenv("LFEM_TILE_ELEMS", str(budget))
+    plan, rp, ci, v = gpu_assemble(m, kinds, coeff=u, variant=lfem.LFEM_NUMERIC_TILED)
+    assert np.array_equal(rp, rp0) and np.array_equal(ci, ci0)
+    for k in kinds:
+        assert np.array_equal(v[k], v0[k]), f"kind {k} differs from the default plan at budget {budget}"
+    o = oracle.assemble_rows(m, kinds, coeff=u)
+    compare_rows(np.arange(m.n_nodes), rp, ci, v, o, kinds)
+
+
+def test_repeated_numeric_calls_reuse_plan_bitwise():
+    """The numeric phase is re-entrant: many calls on one plan (different
+    coefficients, interleaved kind subsets) give the bits of fresh plans."""
+    m = li.make_config("C5", level_override=3)
+    mh = lfem.lfem_mesh_create(m.domain, m.order, m.quad, torch.as_tensor(m.coords, device="cuda"),
+                               torch.as_tensor(m.conn, device="cuda"))
+    plan = lfem.lfem_assemble_symbolic(mh)
+    for seed in range(3):
+        u = li.random_field(m, 100 + seed)
+        cu = torch.as_tensor(u, device="cuda")
+        for kmask in (7, 1, 4, 6, 7):
+            v = [torch.empty(plan.nnz, dtype=torch.float64, device="cuda") if kmask >> i & 1 else None
+                 for i in range(3)]
+            lfem.lfem_assemble_numeric(plan, kmask, cu if kmask & 4 else None, v)
+            lfem.lfem_plan_check(plan)
+            kinds = tuple(k for i, k in enumerate(("M", "A", "Aa")) if kmask >> i & 1)
+            _, _, _, ref = gpu_assemble(m, kinds, coeff=u if kmask & 4 else None)
+            for i, k in enumerate(("M", "A", "Aa")):
+                if kmask >> i & 1:
+                    assert np.array_equal(v[i].cpu().numpy(), ref[k])
