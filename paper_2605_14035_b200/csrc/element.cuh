@@ -254,46 +254,46 @@ struct Elem {
                     g.aq[q] = fma(u, u, 1.0);
                 }
             }
-            return ok;
-        }
+        } else {
 #pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            double J[3][D];
-            jac_at(J0, J1, q, J);
-            if constexpr (D == 2) {
-                const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
-                const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
-                const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
-                const double det = g11 * g22 - g12 * g12;
-                ok &= (det > 0.0) & (det < INFINITY);
-                const double r = rsqrt_nr(det);
-                g.wmu[q] = T.w[q] * (det * r);
-                const double c = T.w[q] * r;
-                g.k11[D == 2 ? q : 0] = c * g22;
-                g.k12[D == 2 ? q : 0] = -c * g12;
-                g.k22[D == 2 ? q : 0] = c * g11;
-            } else {
-                double C[3][3];
-                const double adet = fabs(cof(J, C));
-                ok &= (adet > 0.0) & (adet < INFINITY);
-                g.wmu[q] = T.w[q] * adet;
-            }
-            if (COEF) {
-                double u = 0.0;
-#pragma unroll
-                for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
-                g.aq[q] = fma(u, u, 1.0);
-            }
-        }
-        if constexpr (D == 3) {
-#pragma unroll
-            for (int cc = 0; cc < 3; ++cc)
-#pragma unroll
-                for (int m = 0; m < D; ++m) {
-                    g.J0[cc][m] = J0[cc][m];
-#pragma unroll
-                    for (int n = 0; n < D; ++n) g.J1[cc][m][n] = J1[cc][m][n];
+            for (int q = 0; q < NQ; ++q) {
+                double J[3][D];
+                jac_at(J0, J1, q, J);
+                if constexpr (D == 2) {
+                    const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+                    const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
+                    const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
+                    const double det = g11 * g22 - g12 * g12;
+                    ok &= (det > 0.0) & (det < INFINITY);
+                    const double r = rsqrt_nr(det);
+                    g.wmu[q] = T.w[q] * (det * r);
+                    const double c = T.w[q] * r;
+                    g.k11[D == 2 ? q : 0] = c * g22;
+                    g.k12[D == 2 ? q : 0] = -c * g12;
+                    g.k22[D == 2 ? q : 0] = c * g11;
+                } else {
+                    double C[3][3];
+                    const double adet = fabs(cof(J, C));
+                    ok &= (adet > 0.0) & (adet < INFINITY);
+                    g.wmu[q] = T.w[q] * adet;
                 }
+                if (COEF) {
+                    double u = 0.0;
+#pragma unroll
+                    for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
+                    g.aq[q] = fma(u, u, 1.0);
+                }
+            }
+            if constexpr (D == 3) {
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                    for (int m = 0; m < D; ++m) {
+                        g.J0[cc][m] = J0[cc][m];
+#pragma unroll
+                        for (int n = 0; n < D; ++n) g.J1[cc][m][n] = J1[cc][m][n];
+                    }
+            }
         }
         return ok;
     }
@@ -378,7 +378,7 @@ struct Elem {
                 const double adet = fabs(cof(J, C));
                 double c = T.w[q] * rcp_nr(adet);
                 if (COEF) c = c * g.aq[q];
-                double gr[N][3], h[N][3];
+                double gr[N][3];
 #pragma unroll
                 for (int a = 0; a < N; ++a)
 #pragma unroll
@@ -388,17 +388,16 @@ struct Elem {
                         for (int m = 0; m < D; ++m)
                             if (!S::DZ(a, m)) v = fma(C[k][m], T.dphi[q][a][m], v);
                         gr[a][k] = v;
-                        h[a][k] = c * v;
                     }
 #pragma unroll
                 for (int a = 0; a < N; ++a)
 #pragma unroll
                     for (int b = a; b < N; ++b) {
                         const int s = sym_index(N, a, b);
-                        double st = h[a][0] * gr[b][0];
-                        st = fma(h[a][1], gr[b][1], st);
-                        st = fma(h[a][2], gr[b][2], st);
-                        acc[s] = acc[s] + st;
+                        double st = gr[a][0] * gr[b][0];
+                        st = fma(gr[a][1], gr[b][1], st);
+                        st = fma(gr[a][2], gr[b][2], st);
+                        acc[s] = fma(c, st, acc[s]);
                     }
             }
 #pragma unroll

@@ -27,6 +27,10 @@
 #include "reference.cuh"
 #include "element.cuh"
 
+#ifndef LFEM_V0_TET_MINB
+#define LFEM_V0_TET_MINB 1
+#endif
+
 namespace {
 
 // --------------------------------------------------------------------------
@@ -42,8 +46,11 @@ struct GlobalStageSink {
     __device__ __forceinline__ void operator()(int s, double v) const { stage[base + (int64_t)s * nk] = v; }
 };
 
+template <int F> struct V0Cfg { static constexpr int MINB = 1; };
+template <> struct V0Cfg<FAM_TET_P2> { static constexpr int MINB = LFEM_V0_TET_MINB; };
+
 template <int F, bool DM, bool DA, bool DAA>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, V0Cfg<F>::MINB)
 k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __restrict__ elem_list,
           const double* __restrict__ coords, const double* __restrict__ coeff, double* __restrict__ stage,
           int* __restrict__ err) {
