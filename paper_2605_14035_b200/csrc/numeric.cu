@@ -33,55 +33,80 @@
 
 namespace {
 
+template <int F> struct V0Cfg { static constexpr int MINB = 1; };
+template <> struct V0Cfg<FAM_TET_P2> { static constexpr int MINB = LFEM_V0_TET_MINB; };
+
 // --------------------------------------------------------------------------
 // V0: element kernel -> stage[k][s][le]; slot kernel -> vals
 // --------------------------------------------------------------------------
 // V0 stage, element-major: stage[(le * NS + s) * NK + kr] (kr = rank of the kind among the
 // requested ones), so one contribution's values of all kinds are one vector and the
-// contributions of a CSR row come from a few contiguous element blocks.
-struct GlobalStageSink {
-    double* stage;  // already offset by kr
-    int64_t base;   // le * NS * NK
+// contributions of a CSR row come from a few contiguous element blocks.  Each warp
+// assembles its 32 consecutive elements' blocks in shared memory and writes them as
+// one contiguous range with 16-B stores (a direct per-thread store would scatter
+// every warp store instruction over 32 blocks: LSU-throttled, partial sectors).
+struct SmemStageSink {
+    double* sm;  // this thread's block, already offset by kr
     int nk;
-    __device__ __forceinline__ void operator()(int s, double v) const { stage[base + (int64_t)s * nk] = v; }
+    __device__ __forceinline__ void operator()(int s, double v) const { sm[s * nk] = v; }
 };
 
-template <int F> struct V0Cfg { static constexpr int MINB = 1; };
-template <> struct V0Cfg<FAM_TET_P2> { static constexpr int MINB = LFEM_V0_TET_MINB; };
+constexpr int V0_THREADS = 128;
 
 template <int F, bool DM, bool DA, bool DAA>
-__global__ void __launch_bounds__(128, V0Cfg<F>::MINB)
+constexpr int v0_block_doubles() {
+    return FamInfo<F>::NSYM * ((DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0));
+}
+
+template <int F, bool DM, bool DA, bool DAA>
+__global__ void __launch_bounds__(V0_THREADS, V0Cfg<F>::MINB)
 k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __restrict__ elem_list,
           const double* __restrict__ coords, const double* __restrict__ coeff, double* __restrict__ stage,
           int* __restrict__ err) {
     using E = Elem<F>;
-    constexpr int N = E::N, NS = E::NS, NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
-    for (int64_t le = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; le < n_local;
-         le += (int64_t)gridDim.x * blockDim.x) {
-        double X[N][3], U[N];
+    constexpr int N = E::N, NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
+    constexpr int BD = v0_block_doubles<F, DM, DA, DAA>();  // doubles per element block (even)
+    extern __shared__ __align__(16) double v0_smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* wsm = v0_smem + (size_t)warp * 32 * BD;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t le0 = blockIdx.x * (int64_t)blockDim.x + warp * 32; le0 < n_local; le0 += stride) {
+        const int64_t le = le0 + lane;
+        const int nvalid = n_local - le0 < 32 ? (int)(n_local - le0) : 32;
+        if (le < n_local) {
+            double X[N][3], U[N];
 #pragma unroll
-        for (int a = 0; a < N; ++a) {
-            const int64_t v = __ldg(&lconn[le * N + a]);
+            for (int a = 0; a < N; ++a) {
+                const int64_t v = __ldg(&lconn[le * N + a]);
 #pragma unroll
-            for (int c = 0; c < 3; ++c) X[a][c] = __ldg(&coords[3 * v + c]);
-            U[a] = DAA ? __ldg(&coeff[v]) : 0.0;
+                for (int c = 0; c < 3; ++c) X[a][c] = __ldg(&coords[3 * v + c]);
+                U[a] = DAA ? __ldg(&coeff[v]) : 0.0;
+            }
+            typename E::Geo g;
+            if (!E::template geometry<DAA>(X, U, g)) atomicMin(err, __ldg(&elem_list[le]));
+            double* my = wsm + lane * BD;
+            int kr = 0;
+            if (DM) {
+                SmemStageSink sink{my + kr++, NK};
+                E::template kind<KIND_M>(g, sink);
+            }
+            if (DA) {
+                SmemStageSink sink{my + kr++, NK};
+                E::template kind<KIND_A>(g, sink);
+            }
+            if (DAA) {
+                SmemStageSink sink{my + kr++, NK};
+                E::template kind<KIND_AA>(g, sink);
+            }
         }
-        typename E::Geo g;
-        if (!E::template geometry<DAA>(X, U, g)) atomicMin(err, __ldg(&elem_list[le]));
-        const int64_t base = le * NS * NK;
-        int kr = 0;
-        if (DM) {
-            GlobalStageSink sink{stage + kr++, base, NK};
-            E::template kind<KIND_M>(g, sink);
-        }
-        if (DA) {
-            GlobalStageSink sink{stage + kr++, base, NK};
-            E::template kind<KIND_A>(g, sink);
-        }
-        if (DAA) {
-            GlobalStageSink sink{stage + kr++, base, NK};
-            E::template kind<KIND_AA>(g, sink);
-        }
+        __syncwarp();
+        // contiguous copy of the warp's nvalid blocks (le0 is a multiple of 32: 16-B aligned)
+        const double2* src = reinterpret_cast<const double2*>(wsm);
+        double2* dst = reinterpret_cast<double2*>(stage + le0 * BD);
+        const int nd = nvalid * BD, n2 = nd / 2;
+        for (int i = lane; i < n2; i += 32) dst[i] = src[i];
+        if ((nd & 1) && lane == 0) stage[le0 * BD + nd - 1] = wsm[nd - 1];
+        __syncwarp();
     }
 }
 
@@ -128,7 +153,15 @@ lfem_status run_v0(lfem_plan_s* p, const double* coords, const double* coeff, do
     if (!p->stage) LFEM_TRY(dev_alloc_t(&p->stage, (size_t)3 * NS * p->n_local + 1, s));
     if (p->n_local > 0) {
         prof_begin(p, "k_elem_v0", s);
-        k_elem_v0<F, DM, DA, DAA><<<grid_for(p->n_local, 128, 1 << 20), 128, 0, s>>>(
+        constexpr int BD = v0_block_doubles<F, DM, DA, DAA>();
+        constexpr size_t smem = sizeof(double) * (size_t)V0_THREADS * BD;
+        static bool attr = false;  // per instantiation
+        if (!attr) {
+            LFEM_CUDA(cudaFuncSetAttribute(k_elem_v0<F, DM, DA, DAA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem));
+            attr = true;
+        }
+        k_elem_v0<F, DM, DA, DAA><<<grid_for(p->n_local, V0_THREADS, 1 << 20), V0_THREADS, smem, s>>>(
             p->n_local, p->local_conn, p->elem_list, coords, coeff, p->stage, p->err);
         LFEM_CUDA(cudaGetLastError());
         prof_end(p, s);
