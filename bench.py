@@ -199,10 +199,18 @@ def run_lfem(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         log(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}")
+    # test-only overrides (exercise the multi-rank path on one GPU): LFEM_BENCH_DEVICE pins every rank to
+    # one device, LFEM_BENCH_BACKEND=gloo replaces NCCL (NCCL refuses two ranks on one GPU)
+    if os.environ.get("LFEM_BENCH_DEVICE") is not None:
+        local = int(os.environ["LFEM_BENCH_DEVICE"])
+    backend = os.environ.get("LFEM_BENCH_BACKEND", "nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     name = args.config
 
     # ---- inputs: rank 0 generates (seeded), broadcast over NCCL (plumbing, untimed)
@@ -381,7 +389,9 @@ def run_lfem(args):
         loc = torch.zeros(shard, dtype=torch.float64, device=dev)
         loc[:mine.numel()] = mine
         if world > 1:
-            dist.all_gather_into_tensor(xs, loc)
+            parts = [torch.empty_like(loc) for _ in range(world)]
+            dist.all_gather(parts, loc)
+            xs = torch.cat(parts)
         else:
             xs = loc
         xg = xs[:n_nodes]
