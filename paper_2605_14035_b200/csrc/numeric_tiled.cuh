@@ -34,6 +34,11 @@
 #ifndef LFEM_P1_EPT
 #define LFEM_P1_EPT 4
 #endif
+#ifndef LFEM_P1_RU  // P1 triangles (C3): measured best with 2 chunks per reduce iteration, 176/80 registers
+#define LFEM_P1_RU 2
+#define LFEM_P1_REGS_C 176
+#define LFEM_P1_REGS_R 80
+#endif
 #ifndef LFEM_REGS_C
 #define LFEM_REGS_C 168
 #define LFEM_REGS_R 88
@@ -104,7 +109,7 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 // element budget CW*32*EPT), RU light-slot chunks per reduce iteration,
 // REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default).
 template <int F> struct TileCfg;
-template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_RU, REGS_C = LFEM_RW == 8 ? LFEM_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_REGS_R : 0; };
+template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_P1_RU, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
 template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_RW == 8 ? LFEM_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_REGS_R : 0; };
 template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
