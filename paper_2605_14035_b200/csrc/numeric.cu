@@ -122,7 +122,34 @@ k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* 
         double acc[NK];
 #pragma unroll
         for (int k = 0; k < NK; ++k) acc[k] = 0.0;
-        for (int j = j0; j < j1; ++j) {
+        // four contributions' loads in flight, accumulated in plan order
+        int j = j0;
+        for (; j + 4 <= j1; j += 4) {
+            int c4[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) c4[u] = __ldg(&codes[j + u]);
+            if constexpr (NK == 2) {
+                double2 w4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) w4[u] = __ldg(reinterpret_cast<const double2*>(stage + (int64_t)c4[u] * 2));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    acc[0] += w4[u].x;
+                    acc[1] += w4[u].y;
+                }
+            } else {
+                double w4[4][NK];
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) w4[u][k] = __ldg(stage + (int64_t)c4[u] * NK + k);
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) acc[k] += w4[u][k];
+            }
+        }
+        for (; j < j1; ++j) {
             const double* p = stage + (int64_t)__ldg(&codes[j]) * NK;
             if constexpr (NK == 2) {
                 const double2 w = __ldg(reinterpret_cast<const double2*>(p));

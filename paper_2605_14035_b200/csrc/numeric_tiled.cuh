@@ -39,6 +39,11 @@
 #define LFEM_P1_REGS_C 176
 #define LFEM_P1_REGS_R 80
 #endif
+#ifndef LFEM_P2_CW  // P2 triangles: CTA shape (compute warps, reduce warps, CTAs per SM)
+#define LFEM_P2_CW 8
+#define LFEM_P2_RW 8
+#define LFEM_P2_MINB 1
+#endif
 #ifndef LFEM_REGS_C
 #define LFEM_REGS_C 168
 #define LFEM_REGS_R 88
@@ -49,7 +54,7 @@
 
 namespace {
 
-constexpr int TILE_SMEM_LIMIT = 227 * 1024;
+constexpr int TILE_SMEM_LIMIT = 227 * 1024;  // per SM (divided by the CTAs per SM)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -109,10 +114,10 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 // element budget CW*32*EPT), RU light-slot chunks per reduce iteration,
 // REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default).
 template <int F> struct TileCfg;
-template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_P1_RU, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
-template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = 8, RW = LFEM_RW, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_RW == 8 ? LFEM_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_REGS_R : 0; };
-template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
-template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_P1_RU, MINB = 1, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
+template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
+template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 
 struct TileLayout {
     size_t stage_bytes;           // one stage buffer
@@ -267,7 +272,7 @@ __device__ __forceinline__ void read_nodes(const int4& i2, const uint16_t* s_con
 }
 
 template <int F, bool DM, bool DA, bool DAA>
-__global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, 1) k_tiled(const TileArgs a) {
+__global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCfg<F>::MINB) k_tiled(const TileArgs a) {
     using E = Elem<F>;
     using Cfg = TileCfg<F>;
     constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
@@ -523,7 +528,7 @@ lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
         LFEM_TRY(build_tiles(p, emax, s));
         if (T.ready && T.max_tile_count > tile_capacity<F>())
             return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row touches more elements than the tiled kernel's tile holds");
-        if (T.ready && tile_smem_bytes<F>(T) <= (size_t)TILE_SMEM_LIMIT) break;
+        if (T.ready && tile_smem_bytes<F>(T) <= (size_t)TILE_SMEM_LIMIT / TileCfg<F>::MINB - 1024) break;
         if (emax <= 8 || iter > 16) return lfem_fail(LFEM_ERR_UNSUPPORTED, "no tile size fits the tiled kernel");
         emax = (int)(emax * 0.9);
     }
