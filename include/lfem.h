@@ -191,6 +191,19 @@ lfem_status lfem_profile_read(lfem_plan p, int max, const char** names, double* 
 /* Number of kernel launches lfem_assemble_numeric enqueues for this plan and kinds. */
 int lfem_numeric_launches(lfem_plan p, unsigned kinds);
 
+/* Device-memory allocator hook (a user's caching allocator,
+ * e.g. PyTorch's).  Every device allocation of meshes and plans (plan arrays,
+ * tile plan, V0 stage, e2e staging) goes through alloc(bytes, stream, ctx)
+ * and is released with dealloc(ptr, stream, ctx) on the stream it was used on;
+ * alloc returns a 256-B aligned device pointer or NULL (-> LFEM_ERR_NOMEM).
+ * NULL, NULL restores cudaMalloc / cudaFree.  Process-wide; may be changed at
+ * any time: every pointer is released by the allocator (hook + ctx, or
+ * cudaFree) that produced it.  INVALID_ARG if exactly one of alloc / dealloc
+ * is NULL. */
+typedef void* (*lfem_alloc_fn)(size_t bytes, lfem_stream_t stream, void* ctx);
+typedef void (*lfem_free_fn)(void* ptr, lfem_stream_t stream, void* ctx);
+lfem_status lfem_set_allocator(lfem_alloc_fn alloc, lfem_free_fn dealloc, void* ctx);
+
 int64_t lfem_error_element(void);
 const char* lfem_last_error(void);
 const char* lfem_version(void);

@@ -1,5 +1,7 @@
 // C ABI of liblfem (include/lfem.h): handles, argument checking, errors.
 #include <climits>
+#include <mutex>
+#include <unordered_map>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -104,9 +106,34 @@ lfem_status lfem_cuda_fail(cudaError_t e, const char* what) {
     return lfem_fail(LFEM_ERR_CUDA, std::string(cudaGetErrorString(e)) + " in " + what);
 }
 
+// Device allocations of plans/meshes: cudaMalloc / cudaFree, or the caller's hook
+// (lfem_set_allocator; e.g. PyTorch's caching allocator).  Every pointer is
+// released by the allocator that produced it, even if the hook changed since.
+namespace {
+struct Hook {
+    lfem_alloc_fn alloc = nullptr;
+    lfem_free_fn dealloc = nullptr;
+    void* ctx = nullptr;
+};
+Hook g_hook;
+std::mutex g_hook_mu;
+std::unordered_map<void*, Hook> g_hooked;  // pointers allocated through a hook
+}  // namespace
+
 lfem_status dev_alloc(void** p, size_t bytes, cudaStream_t s) {
-    (void)s;
     *p = nullptr;
+    Hook h;
+    {
+        std::lock_guard<std::mutex> lk(g_hook_mu);
+        h = g_hook;
+    }
+    if (h.alloc) {
+        *p = h.alloc(bytes, reinterpret_cast<lfem_stream_t>(s), h.ctx);
+        if (!*p) return lfem_fail(LFEM_ERR_NOMEM, "allocator hook returned NULL for " + std::to_string(bytes) + " bytes");
+        std::lock_guard<std::mutex> lk(g_hook_mu);
+        g_hooked[*p] = h;
+        return LFEM_OK;
+    }
     cudaError_t e = cudaMalloc(p, bytes);
     if (e != cudaSuccess) {
         cudaGetLastError();
@@ -117,11 +144,34 @@ lfem_status dev_alloc(void** p, size_t bytes, cudaStream_t s) {
 }
 
 void dev_free(void* p, cudaStream_t s) {
-    (void)s;
-    if (p) cudaFree(p);
+    if (!p) return;
+    Hook h;
+    {
+        std::lock_guard<std::mutex> lk(g_hook_mu);
+        auto it = g_hooked.find(p);
+        if (it != g_hooked.end()) {
+            h = it->second;
+            g_hooked.erase(it);
+        }
+    }
+    if (h.dealloc) {
+        h.dealloc(p, reinterpret_cast<lfem_stream_t>(s), h.ctx);
+        return;
+    }
+    cudaFree(p);
 }
 
 extern "C" {
+
+lfem_status lfem_set_allocator(lfem_alloc_fn alloc, lfem_free_fn dealloc, void* ctx) {
+    if ((alloc == nullptr) != (dealloc == nullptr))
+        return lfem_fail(LFEM_ERR_INVALID_ARG, "allocator hook: alloc and dealloc must both be set or both be NULL");
+    std::lock_guard<std::mutex> lk(g_hook_mu);
+    g_hook.alloc = alloc;
+    g_hook.dealloc = dealloc;
+    g_hook.ctx = ctx;
+    return LFEM_OK;
+}
 
 const char* lfem_last_error(void) { return g_err.c_str(); }
 int64_t lfem_error_element(void) { return g_err_elem; }

@@ -33,7 +33,7 @@ EXPORTED = ("lfem_mesh_create", "lfem_mesh_destroy", "lfem_assemble_symbolic", "
             "lfem_plan_info", "lfem_plan_set_variant", "lfem_assemble_numeric", "lfem_assemble_numeric_coords",
             "lfem_assemble_numeric_host", "lfem_csr_get", "lfem_spmv", "lfem_plan_check", "lfem_axpby",
             "lfem_numeric_launches", "lfem_error_element", "lfem_last_error", "lfem_version",
-            "lfem_profile_enable", "lfem_profile_read")
+            "lfem_profile_enable", "lfem_profile_read", "lfem_set_allocator")
 
 
 class LfemError(RuntimeError):
@@ -77,6 +77,7 @@ def _lib():
         L.lfem_error_element.restype = i64
         L.lfem_last_error.restype = ctypes.c_char_p
         L.lfem_version.restype = ctypes.c_char_p
+        L.lfem_set_allocator.argtypes = [vp, vp, vp]
         _LIB = L
     return _LIB
 
@@ -251,6 +252,39 @@ def lfem_profile_read(plan: Plan):
     n = ctypes.c_int()
     _check(_lib().lfem_profile_read(plan.handle, 16, names, ms, cnt, ctypes.byref(n)), "lfem_profile_read")
     return {names[i].decode(): (ms[i], cnt[i]) for i in range(n.value)}
+
+
+ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p)
+_ALLOC_KEEP = []  # keep the ctypes callbacks alive while installed
+
+
+def lfem_set_allocator(alloc=None, dealloc=None) -> None:
+    """Install Python callables alloc(bytes, stream) -> int device pointer and
+    dealloc(ptr, stream) as the library's device allocator (None, None: cudaMalloc)."""
+    if alloc is None and dealloc is None:
+        _check(_lib().lfem_set_allocator(None, None, None), "lfem_set_allocator")
+        _ALLOC_KEEP.clear()
+        return
+    a = ALLOC_FN(lambda n, s, ctx: alloc(int(n), s) or None)
+    f = FREE_FN(lambda p, s, ctx: dealloc(int(p), s))
+    _check(_lib().lfem_set_allocator(a, f, None), "lfem_set_allocator")
+    _ALLOC_KEEP[:] = [a, f]
+
+
+def torch_caching_allocator():
+    """(alloc, dealloc) pair backed by PyTorch's caching allocator on the current device."""
+    live = {}
+
+    def alloc(n, stream):
+        t = torch.empty(max(int(n), 1), dtype=torch.uint8, device="cuda")
+        live[t.data_ptr()] = t
+        return t.data_ptr()
+
+    def dealloc(p, stream):
+        live.pop(int(p), None)
+
+    return alloc, dealloc
 
 
 def lfem_version() -> str:

@@ -242,3 +242,39 @@ def test_repeated_numeric_calls_reuse_plan_bitwise():
             for i, k in enumerate(("M", "A", "Aa")):
                 if kmask >> i & 1:
                     assert np.array_equal(v[i].cpu().numpy(), ref[k])
+
+
+def test_allocator_hook_torch_caching_allocator():
+    """SURVEY §8(b) lfem_set_allocator: plans built through PyTorch's caching
+    allocator give the same bits; every allocation is released with the plan."""
+    import gc
+    m = li.make_config("C5", level_override=3)
+    _, rp0, ci0, v0 = gpu_assemble(m, ("M", "A", "Aa"))
+    alloc, dealloc = lfem.torch_caching_allocator()
+    n = {"a": 0, "f": 0}
+    mine = set()
+
+    def a(nb, s):
+        n["a"] += 1
+        ptr = alloc(nb, s)
+        mine.add(ptr)
+        return ptr
+
+    def f(p, s):
+        assert p in mine, "the hook must only free its own pointers"
+        n["f"] += 1
+        dealloc(p, s)
+
+    lfem.lfem_set_allocator(a, f)
+    try:
+        plan, rp, ci, v = gpu_assemble(m, ("M", "A", "Aa"))
+        assert n["a"] > 0
+        assert np.array_equal(rp, rp0) and np.array_equal(ci, ci0)
+        for k in ("M", "A", "Aa"):
+            assert np.array_equal(v[k], v0[k])
+        del plan
+        gc.collect()
+        torch.cuda.synchronize()
+    finally:
+        lfem.lfem_set_allocator(None, None)
+    assert n["f"] == n["a"], n

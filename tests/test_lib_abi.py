@@ -60,3 +60,13 @@ def test_version_without_gpu(libpath):
     lib = ctypes.CDLL(libpath)
     lib.lfem_version.restype = ctypes.c_char_p
     assert b"sm_100a" in lib.lfem_version()
+
+
+def test_allocator_hook_argument_check_without_gpu(libpath):
+    """lfem_set_allocator: both callbacks or neither (no device call involved)."""
+    lib = ctypes.CDLL(libpath)
+    lib.lfem_set_allocator.argtypes = [ctypes.c_void_p] * 3
+    ALLOC = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+    a = ALLOC(lambda n, s, c: None)
+    assert lib.lfem_set_allocator(ctypes.cast(a, ctypes.c_void_p), None, None) == 1  # INVALID_ARG
+    assert lib.lfem_set_allocator(None, None, None) == 0
