@@ -49,7 +49,9 @@
  *    reading G21).  No floating-point atomics anywhere.
  *  - Limits: n_nodes, n_elems < 2^31; local entries n_elems_local*nref^2 < 2^31;
  *    per row at most 512 candidate (element, column) entries (a P2 tet vertex
- *    shared by <= 51 tets); violations return LFEM_ERR_UNSUPPORTED.
+ *    shared by <= 51 tets); TILED: a row may touch at most the tile capacity
+ *    of elements (256 P2 / 1024 P1 triangles, 128 P2 / 256 P1 tets) and a CSR
+ *    slot at most 254 contributions; violations return LFEM_ERR_UNSUPPORTED.
  */
 #ifndef LFEM_H_
 #define LFEM_H_
@@ -92,11 +94,13 @@ typedef enum {
 /* 'kinds' bitmask of lfem_assemble_numeric; vals[] index = bit position. */
 enum { LFEM_MASS = 1u, LFEM_STIFF = 2u, LFEM_STIFF_COEF = 4u };
 
-/* Numeric variants (lfem_plan_set_variant); all produce identical bits. */
+/* Numeric variants (lfem_plan_set_variant); all produce identical bits.
+ * AUTO picks TILED for triangles and V0 for tetrahedra (measured). */
 typedef enum {
     LFEM_NUMERIC_AUTO = 0,   /* the fastest measured variant for the family */
-    LFEM_NUMERIC_V0 = 1,     /* element kernel -> staged local matrices -> per-slot gather */
-    LFEM_NUMERIC_TILED = 2   /* fused row-tile kernel (shared-memory staging, halo recompute) */
+    LFEM_NUMERIC_V0 = 1,     /* element kernel -> element-major local matrices in HBM -> per-slot gather */
+    LFEM_NUMERIC_TILED = 2   /* fused row-tile kernel: TMA-fed, warp-specialised, shared-memory stage,
+                                halo recompute; the tile plan is built on the first call (one sync) */
 } lfem_numeric_variant;
 
 typedef struct lfem_mesh_s* lfem_mesh;

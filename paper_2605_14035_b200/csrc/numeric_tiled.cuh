@@ -520,9 +520,18 @@ lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
     TilePlan& T = p->tiles;
     if (T.ready) return LFEM_OK;
     int emax = tile_capacity<F>();
+    // tiny meshes (fewer elements than ~2 full tiles per SM): smaller tiles spread them over the SMs
+    // (a tile's pipeline latency, not its work, sets the time there)
+    int dev = 0, sms = 148;
+    LFEM_CUDA(cudaGetDevice(&dev));
+    LFEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    if (p->n_local < (int64_t)emax * sms * 2) {
+        const int64_t e = (p->n_local + sms - 1) / sms;
+        emax = (int)(e < 32 ? 32 : (e > emax ? emax : e));
+    }
     if (const char* env = std::getenv("LFEM_TILE_ELEMS")) {
         const int r = std::atoi(env);
-        if (r >= 8 && r < emax) emax = r;
+        if (r >= 8 && r < tile_capacity<F>()) emax = r;
     }
     for (int iter = 0;; ++iter) {
         LFEM_TRY(build_tiles(p, emax, s));
