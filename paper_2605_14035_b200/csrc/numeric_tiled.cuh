@@ -39,13 +39,23 @@
 #define LFEM_P1_REGS_C 176
 #define LFEM_P1_REGS_R 80
 #endif
-#ifndef LFEM_P2_CW  // P2 triangles: CTA shape (compute warps, reduce warps, CTAs per SM)
+// P2 triangles: CTA shape (compute warps, reduce warps, CTAs per SM, elements per compute thread)
+#ifndef LFEM_P2_CW
 #define LFEM_P2_CW 8
+#endif
+#ifndef LFEM_P2_RW
 #define LFEM_P2_RW 8
+#endif
+#ifndef LFEM_P2_MINB
 #define LFEM_P2_MINB 1
+#endif
+#ifndef LFEM_P2_EPT
+#define LFEM_P2_EPT 1
 #endif
 #ifndef LFEM_REGS_C
 #define LFEM_REGS_C 168
+#endif
+#ifndef LFEM_REGS_R
 #define LFEM_REGS_R 88
 #endif
 #ifndef LFEM_RU
@@ -115,7 +125,7 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 // REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default).
 template <int F> struct TileCfg;
 template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_P1_RU, MINB = 1, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
-template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = 1, RU = LFEM_RU, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
+template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = LFEM_P2_EPT, RU = LFEM_RU, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
 template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 
