@@ -58,6 +58,9 @@
 #ifndef LFEM_REGS_R
 #define LFEM_REGS_R 88
 #endif
+#ifndef LFEM_NSB  // stage buffers (kind passes in flight between compute and reduce warps)
+#define LFEM_NSB 2
+#endif
 #ifndef LFEM_RU
 #define LFEM_RU 4
 #endif
@@ -148,7 +151,7 @@ __host__ __device__ inline TileLayout tile_layout(int nsym, int nref, int maxe, 
     L.xyz_off = 0;
     L.u_off = align16(sizeof(double) * (3 * (size_t)nodes_cap + 2));
     L.node_bytes = L.u_off + align16(sizeof(double) * ((size_t)nodes_cap + 2));
-    size_t o = 2 * L.stage_bytes;
+    size_t o = LFEM_NSB * L.stage_bytes;
     for (int b = 0; b < 3; ++b) L.meta_off[b] = o + b * L.meta_bytes;
     o += 3 * L.meta_bytes;
     for (int b = 0; b < 2; ++b) L.node_off[b] = o + b * L.node_bytes;
@@ -288,7 +291,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
     constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
     unsigned char* smem = reinterpret_cast<unsigned char*>(tile_smem_d);
     __shared__ int meta_done[3];  // reduce warps done with the tile in meta buffer b
-    __shared__ __align__(8) uint64_t meta_full[3], stage_full[2], stage_empty[2], node_full[2],
+    __shared__ __align__(8) uint64_t meta_full[3], stage_full[LFEM_NSB], stage_empty[LFEM_NSB], node_full[2],
         node_empty[2];
     __shared__ int4 sinfo[3][3];
 
@@ -302,9 +305,11 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
             mbar_init(&meta_full[b], 1);
             meta_done[b] = 0;
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int b = 0; b < LFEM_NSB; ++b) {
             mbar_init(&stage_full[b], CT);
             mbar_init(&stage_empty[b], RW * 32);
+        }
+        for (int b = 0; b < 2; ++b) {
             mbar_init(&node_full[b], 1 + CT);
             mbar_init(&node_empty[b], CT);
         }
@@ -361,9 +366,10 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
             }
             // one kind per stage pass: wait for a free stage buffer, store, hand it to the reduce warps
 #define LFEM_STAGE_ACQUIRE()                                                   \
-    const int sb_ = pass & 1;                                                  \
+    const int sb_ = pass % LFEM_NSB;                                           \
+    const uint32_t use_ = pass / LFEM_NSB;                                     \
     pc.lap(a.dbg, 3);                                                          \
-    if ((pass >> 1) > 0) mbar_wait(&stage_empty[sb_], ((pass >> 1) - 1) & 1);  \
+    if (use_ > 0) mbar_wait(&stage_empty[sb_], (use_ - 1) & 1);                \
     pc.lap(a.dbg, 4);                                                          \
     double* st = tile_smem_d + sb_ * stage_dbl;                                \
     const bool do_store = !(a.debug & 1)
@@ -434,9 +440,9 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
 #pragma unroll
             for (int kind = 0; kind < 3; ++kind) {
                 if ((kind == KIND_M && !DM) || (kind == KIND_A && !DA) || (kind == KIND_AA && !DAA)) continue;
-                const int sb = pass & 1;
+                const int sb = pass % LFEM_NSB;
                 pc.lap(a.dbg, 8);
-                mbar_wait(&stage_full[sb], (pass >> 1) & 1);
+                mbar_wait(&stage_full[sb], (pass / LFEM_NSB) & 1);
                 pc.lap(a.dbg, 10);  // wait for a full stage
                 const double* st = tile_smem_d + sb * stage_dbl;
                 double* out = a.v[kind] + s0;
