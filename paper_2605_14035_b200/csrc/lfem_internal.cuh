@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <vector>
 
 #include "../../include/lfem.h"
 
@@ -101,6 +102,33 @@ template <class T>
 inline lfem_status dev_alloc_t(T** p, size_t n, cudaStream_t s) {
     return dev_alloc(reinterpret_cast<void**>(p), n * sizeof(T) + 16, s);
 }
+
+// Device temporaries of a host function: track() them after declaring,
+// drop() frees early; whatever is still held is freed on every exit path
+// (including early error returns).  give() hands ownership to the caller.
+struct DevScope {
+    cudaStream_t s;
+    std::vector<void**> ptrs;
+    explicit DevScope(cudaStream_t st) : s(st) {}
+    DevScope(const DevScope&) = delete;
+    DevScope& operator=(const DevScope&) = delete;
+    template <class T> void track(T** p) { ptrs.push_back(reinterpret_cast<void**>(p)); }
+    template <class T> void drop(T*& p) {
+        dev_free(p, s);
+        p = nullptr;
+    }
+    template <class T> void give(T** p) {
+        for (auto& q : ptrs)
+            if (q == reinterpret_cast<void**>(p)) q = nullptr;
+    }
+    ~DevScope() {
+        for (void** q : ptrs)
+            if (q && *q) {
+                dev_free(*q, s);
+                *q = nullptr;
+            }
+    }
+};
 
 // scan.cu: out[0] = 0, out[i+1] = sum_{j<=i} in[j]  (n+1 outputs)
 lfem_status scan_exclusive_i32_to_i64(const int32_t* in, int64_t* out, int64_t n, cudaStream_t s);

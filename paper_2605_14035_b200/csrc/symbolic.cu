@@ -179,10 +179,13 @@ inline unsigned grid_for(int64_t n, int threads) {
 // inc_ptr[r+1]) = the local entries i = e_local * nref + a with conn[e, a] = r,
 // ascending (counting sort by row, then a per-row insertion sort).
 lfem_status build_incidence(lfem_plan_s* p, int64_t** inc_ptr_out, int32_t** inc_out, cudaStream_t s) {
+    DevScope scope(s);
     const int nref = p->mesh->nref;
     const int64_t rb = p->row_begin, re = p->row_end, n_rows = re - rb, n_local = p->n_local;
     int32_t* cnt = nullptr;
+    scope.track(&cnt);
     int64_t* inc_ptr = nullptr;
+    scope.track(&inc_ptr);
     LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
     LFEM_TRY(dev_alloc_t(&inc_ptr, n_rows + 1, s));
     LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
@@ -195,6 +198,7 @@ lfem_status build_incidence(lfem_plan_s* p, int64_t** inc_ptr_out, int32_t** inc
     LFEM_CUDA(cudaMemcpyAsync(&total_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
     int32_t* inc = nullptr;
+    scope.track(&inc);
     LFEM_TRY(dev_alloc_t(&inc, total_inc + 1, s));
     LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_rows + 1), s));
     if (n_local > 0) {
@@ -205,20 +209,25 @@ lfem_status build_incidence(lfem_plan_s* p, int64_t** inc_ptr_out, int32_t** inc
         k_sort_inc<<<grid_for(n_rows, 128), 128, 0, s>>>(inc_ptr, n_rows, inc);
         LFEM_CUDA(cudaGetLastError());
     }
-    dev_free(cnt, s);
+    scope.drop(cnt);
+    scope.give(&inc_ptr);
     *inc_ptr_out = inc_ptr;
+    scope.give(&inc);
     *inc_out = inc;
     return LFEM_OK;
 }
 
 lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
+    DevScope scope(s);
     const lfem_mesh_s* m = p->mesh;
     const int nref = m->nref;
     const int64_t rb = p->row_begin, re = p->row_end, n_rows = re - rb;
     p->n_rows = n_rows;
     // 1. elements touching the owned rows
     int32_t* flag = nullptr;
+    scope.track(&flag);
     int64_t* pos = nullptr;
+    scope.track(&pos);
     LFEM_TRY(dev_alloc_t(&flag, m->n_elems + 1, s));
     LFEM_TRY(dev_alloc_t(&pos, m->n_elems + 1, s));
     if (m->n_elems > 0) {
@@ -239,11 +248,13 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
                                                             p->local_conn);
         LFEM_CUDA(cudaGetLastError());
     }
-    dev_free(flag, s);
-    dev_free(pos, s);
+    scope.drop(flag);
+    scope.drop(pos);
     // 2. counting sort of local rows by global row
     int64_t* inc_ptr = nullptr;
+    scope.track(&inc_ptr);
     int32_t* inc = nullptr;
+    scope.track(&inc);
     LFEM_TRY(build_incidence(p, &inc_ptr, &inc, s));
     int64_t total_inc = 0;
     LFEM_CUDA(cudaMemcpyAsync(&total_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -252,9 +263,11 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     if (p->n_contrib >= (int64_t)INT_MAX)
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "contributions >= 2^31");
     int32_t* cnt = nullptr;
+    scope.track(&cnt);
     LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
     // 3. row lengths
     int* overflow = nullptr;
+    scope.track(&overflow);
     LFEM_TRY(dev_alloc_t(&overflow, 1, s));
     LFEM_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(n_rows, ROW_WARPS);
@@ -284,10 +297,10 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     }
     k_set_last<<<1, 1, 0, s>>>(p->slot_ptr, p->nnz, p->n_contrib);
     LFEM_CUDA(cudaGetLastError());
-    dev_free(cnt, s);
-    dev_free(inc_ptr, s);
-    dev_free(inc, s);
-    dev_free(overflow, s);
+    scope.drop(cnt);
+    scope.drop(inc_ptr);
+    scope.drop(inc);
+    scope.drop(overflow);
     LFEM_CUDA(cudaStreamSynchronize(s));
     return LFEM_OK;
 }

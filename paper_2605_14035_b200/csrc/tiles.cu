@@ -342,6 +342,7 @@ __global__ void k_tile_info(int n_tiles, int64_t rb, const int64_t* __restrict__
 }  // namespace
 
 lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
+    DevScope scope(s);
     free_tiles(p->tiles, s);
     TilePlan& T = p->tiles;
     const int nref = p->mesh->nref;
@@ -352,16 +353,23 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     }
     // greedy element-budget partition (see the header)
     int64_t* inc_ptr = nullptr;
+    scope.track(&inc_ptr);
     int32_t* inc = nullptr;
+    scope.track(&inc);
     LFEM_TRY(build_incidence(p, &inc_ptr, &inc, s));
     int64_t n_inc = 0;
     LFEM_CUDA(cudaMemcpyAsync(&n_inc, inc_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
     int32_t* prev = nullptr;
+    scope.track(&prev);
     int32_t* start = nullptr;
+    scope.track(&start);
     int64_t* spos = nullptr;
+    scope.track(&spos);
     int32_t* tile_of = nullptr;
+    scope.track(&tile_of);
     int* flags = nullptr;  // [0] overflow/bad, [1] max elems, [2] max slots, [3] max heavy
+    scope.track(&flags);
     LFEM_TRY(dev_alloc_t(&prev, n_inc + 1, s));
     LFEM_TRY(dev_alloc_t(&start, n_rows + 1, s));
     LFEM_TRY(dev_alloc_t(&spos, n_rows + 1, s));
@@ -389,22 +397,25 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     LFEM_CUDA(cudaMemcpyAsync(&nt64, spos + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaMemcpyAsync(&hbad, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
-    dev_free(inc_ptr, s);
-    dev_free(inc, s);
-    dev_free(prev, s);
+    scope.drop(inc_ptr);
+    scope.drop(inc);
+    scope.drop(prev);
     if (hbad) return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row touches more elements than a tile holds");
     if (nt64 >= INT_MAX / 2) return lfem_fail(LFEM_ERR_UNSUPPORTED, "too many tiles");
     const int n_tiles = (int)nt64;
     int64_t* bounds = nullptr;
+    scope.track(&bounds);
     int32_t* cnt = nullptr;
+    scope.track(&cnt);
     int64_t* ptr = nullptr;
+    scope.track(&ptr);
     LFEM_TRY(dev_alloc_t(&bounds, n_tiles + 1, s));
     LFEM_TRY(dev_alloc_t(&cnt, n_tiles + 1, s));
     LFEM_TRY(dev_alloc_t(&ptr, n_tiles + 1, s));
     k_tile_bounds<<<grid_for(n_rows, 256), 256, 0, s>>>(n_rows, start, spos, bounds, tile_of);
     LFEM_CUDA(cudaGetLastError());
-    dev_free(start, s);
-    dev_free(spos, s);
+    scope.drop(start);
+    scope.drop(spos);
     LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_tiles + 1), s));
     if (n_local > 0) {
         k_tile_count<<<grid_for(n_local, 256), 256, 0, s>>>(p->local_conn, n_local, nref, p->row_begin, p->row_end,
@@ -415,6 +426,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     T.n_tiles = n_tiles;
     T.rows_per_tile = (int)((n_rows + n_tiles - 1) / n_tiles);  // average (reporting only)
     int32_t* tmp = nullptr;
+    scope.track(&tmp);
     int64_t total = 0;
     LFEM_CUDA(cudaMemcpyAsync(&total, ptr + n_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
@@ -433,22 +445,23 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     int h[4] = {0, 0, 0, 0};
     LFEM_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
-    dev_free(tmp, s);
+    scope.drop(tmp);
     if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile element list too long");
     // stage stride: odd, so the nsym entries of one element fall in different smem banks
     const int maxe = (h[1] > 0 ? h[1] : 1) | 1;
     T.max_tile_elems = maxe;
     T.max_tile_count = h[1];
     if ((int64_t)p->mesh->nsym * maxe >= 0xffff) {  // 16-bit codes: the caller lowers the budget
-        dev_free(cnt, s);
-        dev_free(ptr, s);
-        dev_free(flags, s);
-        dev_free(bounds, s);
-        dev_free(tile_of, s);
+        scope.drop(cnt);
+        scope.drop(ptr);
+        scope.drop(flags);
+        scope.drop(bounds);
+        scope.drop(tile_of);
         return LFEM_OK;
     }
     // halo nodes per tile (pass 0: counts)
     int32_t* hcnt = nullptr;
+    scope.track(&hcnt);
     LFEM_TRY(dev_alloc_t(&hcnt, n_tiles + 1, s));
     const unsigned node_grid = n_tiles < 148 * 8 ? n_tiles : 148 * 8;
     k_tile_nodes<0><<<node_grid, 256, 0, s>>>(n_tiles, nref, p->row_begin, bounds, ptr, T.tile_elems, p->local_conn,
@@ -456,8 +469,11 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     LFEM_CUDA(cudaGetLastError());
     // element / connectivity / halo offsets as int32 (host; n_tiles is small)
     int32_t* eptr32 = nullptr;
+    scope.track(&eptr32);
     int32_t* cptr32 = nullptr;
+    scope.track(&cptr32);
     int32_t* lptr32 = nullptr;
+    scope.track(&lptr32);
     {
         std::vector<int64_t> hp(n_tiles + 1);
         std::vector<int32_t> hp32(n_tiles + 1), cp(n_tiles + 1), hc(n_tiles + 1), lp(n_tiles + 1);
@@ -493,7 +509,9 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     }
     // heavy entries: per-row heavy-slot counts -> global entry offsets; entry size from the largest count
     int32_t* hu = nullptr;
+    scope.track(&hu);
     int64_t* hptr = nullptr;
+    scope.track(&hptr);
     LFEM_TRY(dev_alloc_t(&hu, n_rows + 1, s));
     LFEM_TRY(dev_alloc_t(&hptr, n_rows + 1, s));
     LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
@@ -526,17 +544,17 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     LFEM_CUDA(cudaGetLastError());
     LFEM_CUDA(cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
-    dev_free(cnt, s);
-    dev_free(ptr, s);
-    dev_free(flags, s);
-    dev_free(hu, s);
-    dev_free(hptr, s);
-    dev_free(eptr32, s);
-    dev_free(cptr32, s);
-    dev_free(lptr32, s);
-    dev_free(hcnt, s);
-    dev_free(bounds, s);
-    dev_free(tile_of, s);
+    scope.drop(cnt);
+    scope.drop(ptr);
+    scope.drop(flags);
+    scope.drop(hu);
+    scope.drop(hptr);
+    scope.drop(eptr32);
+    scope.drop(cptr32);
+    scope.drop(lptr32);
+    scope.drop(hcnt);
+    scope.drop(bounds);
+    scope.drop(tile_of);
     if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile code construction failed (" + std::to_string(h[0]) + ")");
     T.max_tile_slots = h[2];
     T.max_tile_heavy = h[3];
