@@ -278,3 +278,59 @@ def test_allocator_hook_torch_caching_allocator():
     finally:
         lfem.lfem_set_allocator(None, None)
     assert n["f"] == n["a"], n
+
+
+# ---------------------------------------------------------------------------- mesh-shape edge cases
+def _fan(nseg, order, rings=2):
+    """Disk-like surface fan around one vertex of valence nseg (nseg up to 40: slots with up to
+    40 contributions -> the tiled kernel's larger heavy entries), a second ring for more rows,
+    slightly curved in z."""
+    pts = [[0.0, 0.0, 0.0]]
+    for r in range(1, rings + 1):
+        for k in range(nseg):
+            t = 2 * np.pi * (k + 0.5 * (r - 1)) / nseg
+            pts.append([r * np.cos(t), r * np.sin(t), 0.05 * r * r])
+    tris = []
+    for k in range(nseg):
+        tris.append([0, 1 + k, 1 + (k + 1) % nseg])
+    for r in range(1, rings):
+        a0, b0 = 1 + (r - 1) * nseg, 1 + r * nseg
+        for k in range(nseg):
+            a, a1 = a0 + k, a0 + (k + 1) % nseg
+            b, b1 = b0 + k, b0 + (k + 1) % nseg
+            tris += [[a, b, a1], [a1, b, b1]]
+    v, f = np.array(pts), np.array(tris)
+    if order == 2:
+        v, f = li.p2_from_p1_triangles(v, f, project_sphere=False)
+        return li.Mesh(li.SURFACE_TRI, 2, v, f.astype(np.int32), li.QUAD_TRI6_DEG4)
+    return li.Mesh(li.SURFACE_TRI, 1, v, f.astype(np.int32), li.QUAD_TRI3_DEG2)
+
+
+@pytest.mark.parametrize("variant", [lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED], ids=["v0", "tiled"])
+@pytest.mark.parametrize("nseg,order", [(7, 1), (13, 1), (40, 1), (9, 2), (30, 2)])
+def test_high_valence_fans(nseg, order, variant):
+    """Vertex valences 7..40 (icospheres have <= 6): heavy slots with up to 40
+    contributions (16-, 32- and 64-word heavy entries in the tiled kernel)."""
+    m = li._finish(_fan(nseg, order))
+    u = li.random_field(m, 7)
+    worst, _ = check_full(m, ("M", "A", "Aa"), coeff=u, variant=variant)
+    assert worst <= TOL
+
+
+@pytest.mark.parametrize("variant", [lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED], ids=["v0", "tiled"])
+def test_unreferenced_nodes_give_empty_rows(variant):
+    """Nodes no element uses (interleaved with used ones) are empty CSR rows:
+    row_ptr repeats, the tiles around them stay correct."""
+    base = li.make_config("C5", level_override=2)
+    n = base.n_nodes
+    # new numbering: every 3rd new id is an unused node
+    new_id = np.arange(n) + np.arange(n) // 2
+    coords = np.zeros((n + (n - 1) // 2 + 1, 3))
+    coords[new_id] = base.coords
+    unused = np.setdiff1d(np.arange(coords.shape[0]), new_id)
+    coords[unused] = np.random.default_rng(0).normal(size=(unused.size, 3))
+    m = li._finish(li.Mesh(base.domain, base.order, coords, new_id[base.conn].astype(np.int32), base.quad))
+    u = li.random_field(m, 3)
+    worst, (plan, rp, ci, vals) = check_full(m, ("M", "A", "Aa"), coeff=u, variant=variant)
+    assert worst <= TOL
+    assert np.all(np.diff(rp)[unused] == 0)
