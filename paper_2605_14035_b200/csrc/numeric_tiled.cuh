@@ -62,7 +62,7 @@
 #define LFEM_NSB 2
 #endif
 #ifndef LFEM_RU
-#define LFEM_RU 4
+#define LFEM_RU 3  // light chunks per reduce iteration (P2): measured 3 > 4 > 2 > 5, 8 on C5
 #endif
 
 namespace {
