@@ -119,20 +119,23 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
 def _oracle_rows_for(m, kinds, coeff, target_s, nt):
-    """Rows of a contiguous block that take about target_s seconds in the oracle:
-    two calibration runs separate the per-call setup from the per-row cost."""
+    """Rows of a contiguous block that take about target_s seconds in the oracle.
+    The oracle has a per-call setup (node -> element incidence over the whole
+    mesh) and a per-row cost: a tiny sample measures the first, a 5 % sample the
+    second; the per-row cost grows with the sample (map sizes, caches), hence a
+    safety factor of 1.7 (measured on C5 at level 8: 0.8 us/row at 2 %, 1.35 at 100 %)."""
     import oracle
-    r1 = min(m.n_nodes, 20000)
-    r2 = min(m.n_nodes, 2 * r1)
+    r0 = min(m.n_nodes, 100)
+    r1 = min(m.n_nodes, max(50000, m.n_nodes // 20))
+    t0 = time.perf_counter()
+    oracle.assemble_rows(m, kinds, rows=np.arange(r0, dtype=np.int64), coeff=coeff, nthreads=nt)
+    setup = time.perf_counter() - t0
     t0 = time.perf_counter()
     oracle.assemble_rows(m, kinds, rows=np.arange(r1, dtype=np.int64), coeff=coeff, nthreads=nt)
     t1 = time.perf_counter() - t0
-    t0 = time.perf_counter()
-    oracle.assemble_rows(m, kinds, rows=np.arange(r2, dtype=np.int64), coeff=coeff, nthreads=nt)
-    t2 = time.perf_counter() - t0
-    per_row = max((t2 - t1) / max(1, r2 - r1), 1e-9)
-    rows = int(r2 + max(0.0, target_s - t2) / per_row)
-    return int(min(m.n_nodes, max(r1, rows)))
+    per_row = max((t1 - setup) / max(1, r1 - r0), t1 / r1 * 1e-3, 1e-9)
+    rows = int(r0 + max(0.0, target_s - setup) / (1.7 * per_row))
+    return int(min(m.n_nodes, max(r0, rows)))
 
 
 def oracle_sample(m, kinds, coeff, target_s):

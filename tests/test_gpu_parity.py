@@ -334,3 +334,4 @@ def test_unreferenced_nodes_give_empty_rows(variant):
     worst, (plan, rp, ci, vals) = check_full(m, ("M", "A", "Aa"), coeff=u, variant=variant)
     assert worst <= TOL
     assert np.all(np.diff(rp)[unused] == 0)
+
