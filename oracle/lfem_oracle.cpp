@@ -32,6 +32,18 @@
 //      when conn[e,a] is a requested row;
 //   3. the map's (row, col) order is CSR order (explicit zeros kept, G19).
 // Per-slot summation order: ascending element id, then (a, b) (reading G21).
+//
+// Right-hand sides, for every requested row j:
+//   load:  b_j = sum_{E ∋ j} sum_q w_q mu_E(xi_q) f_h(xi_q) phi_j(xi_q),
+//          f_h = sum_c f_c phi_c  (Eq. "load vector" P:168-177; with the
+//          element rule this is exactly b = M f)
+//   KLL:   with u = (nu_1, nu_2, nu_3, H) nodal (u = (n; H)),
+//          alpha^2(xi_q) = |grad_Gamma_h nu_h|^2 = sum_k |sum_c nu_{c,k} g_c|^2
+//          (Frobenius norm, Listing 2 line 2),
+//          f_{k,j} = sum_E sum_q w_q mu alpha^2 u_{h,k}(xi_q) phi_j(xi_q),
+//          k = 1..4 (f_1 = first three, f_2 = H component; P:784-789,
+//          Listing 2 lines 3-4).  Surfaces only.
+// Per-row summation order: ascending element id (one entry per element).
 // Degenerate element (mu <= 0 or non-finite at a quadrature point) or a node
 // index out of range -> error code with the lowest offending element id.
 //
@@ -240,64 +252,80 @@ bool inv3(const double A[3][3], double Ai[3][3], double* det_out) {
     return true;
 }
 
+// J (3 x d) at quadrature point q: column m = sum_{j>=2} (x_j - x_1) dphi_j/dxi_m
+void jacobian(const Ref& R, const double* X /* nref x 3 */, size_t q, double J[3][3]) {
+    const int n = R.nref, d = R.d;
+    for (int c = 0; c < 3; ++c) J[c][0] = J[c][1] = J[c][2] = 0.0;
+    for (int j = 1; j < n; ++j)
+        for (int c = 0; c < 3; ++c)
+            for (int m = 0; m < d; ++m)
+                J[c][m] += (X[3 * j + c] - X[c]) * R.grad[q][j][m];
+}
+
+// Measure mu and the gradients g[a] (3-vectors) of the basis at quadrature
+// point q from the Jacobian J (3 x d):
 // formulation 0: the north star's  g = J G^{-1} grad (surface), J^{-T} grad (bulk)
 // formulation 1: Listing 1's  g = L^{-T} [grad; 0] with L = [t1 t2 t1 x t2]
 //                (columns; reading G2) -- surfaces only; used as a second,
 //                independent formulation by the brute-force pin.
+int point_gradients(const Ref& R, const double J[3][3], size_t q, int formulation, double* mu, double g[10][3]) {
+    const int n = R.nref, d = R.d;
+    if (d == 2) {
+        double G[2][2];
+        for (int a = 0; a < 2; ++a)
+            for (int b = 0; b < 2; ++b) {
+                G[a][b] = 0.0;
+                for (int c = 0; c < 3; ++c) G[a][b] += J[c][a] * J[c][b];
+            }
+        const double detG = G[0][0] * G[1][1] - G[0][1] * G[1][0];
+        *mu = std::sqrt(detG);
+        if (!(*mu > 0.0) || !std::isfinite(*mu)) return ERR_DEGENERATE;
+        if (formulation == 0) {
+            const double Gi[2][2] = {{G[1][1] / detG, -G[0][1] / detG},
+                                     {-G[1][0] / detG, G[0][0] / detG}};
+            for (int a = 0; a < n; ++a) {
+                double s[2];
+                for (int m = 0; m < 2; ++m)
+                    s[m] = Gi[m][0] * R.grad[q][a][0] + Gi[m][1] * R.grad[q][a][1];
+                for (int c = 0; c < 3; ++c) g[a][c] = J[c][0] * s[0] + J[c][1] * s[1];
+            }
+        } else {
+            double L[3][3], Li[3][3], dummy;
+            const double nrm[3] = {J[1][0] * J[2][1] - J[2][0] * J[1][1],
+                                   J[2][0] * J[0][1] - J[0][0] * J[2][1],
+                                   J[0][0] * J[1][1] - J[1][0] * J[0][1]};
+            for (int c = 0; c < 3; ++c) { L[c][0] = J[c][0]; L[c][1] = J[c][1]; L[c][2] = nrm[c]; }
+            if (!inv3(L, Li, &dummy)) return ERR_DEGENERATE;
+            for (int a = 0; a < n; ++a)
+                for (int c = 0; c < 3; ++c)  // (L^{-T} v)_c = sum_k Li[k][c] v_k
+                    g[a][c] = Li[0][c] * R.grad[q][a][0] + Li[1][c] * R.grad[q][a][1];
+        }
+    } else {
+        double Ji[3][3], det;
+        if (!inv3(J, Ji, &det)) return ERR_DEGENERATE;
+        *mu = std::fabs(det);
+        if (!(*mu > 0.0) || !std::isfinite(*mu)) return ERR_DEGENERATE;
+        for (int a = 0; a < n; ++a)
+            for (int c = 0; c < 3; ++c)  // (J^{-T} v)_c = sum_k Ji[k][c] v_k
+                g[a][c] = Ji[0][c] * R.grad[q][a][0] + Ji[1][c] * R.grad[q][a][1] +
+                          Ji[2][c] * R.grad[q][a][2];
+    }
+    return OK;
+}
+
+// Full local matrices; formulation as in point_gradients.
 int element_matrices(const Ref& R, const double* X /* nref x 3 */, const double* u /* nref or null */,
                      int formulation, double* Ml, double* Al, double* Aal) {
-    const int n = R.nref, d = R.d;
+    const int n = R.nref;
     for (int i = 0; i < n * n; ++i) { Ml[i] = 0.0; Al[i] = 0.0; Aal[i] = 0.0; }
     for (size_t q = 0; q < R.rule.size(); ++q) {
         const double w = R.rule[q].w;
-        // J (3 x d): column m = sum_{j>=2} (x_j - x_1) dphi_j/dxi_m
-        double J[3][3] = {{0, 0, 0}, {0, 0, 0}, {0, 0, 0}};
-        for (int j = 1; j < n; ++j)
-            for (int c = 0; c < 3; ++c)
-                for (int m = 0; m < d; ++m)
-                    J[c][m] += (X[3 * j + c] - X[c]) * R.grad[q][j][m];
+        double J[3][3];
+        jacobian(R, X, q, J);
         double mu = 0.0;
         double g[10][3];
-        if (d == 2) {
-            double G[2][2];
-            for (int a = 0; a < 2; ++a)
-                for (int b = 0; b < 2; ++b) {
-                    G[a][b] = 0.0;
-                    for (int c = 0; c < 3; ++c) G[a][b] += J[c][a] * J[c][b];
-                }
-            const double detG = G[0][0] * G[1][1] - G[0][1] * G[1][0];
-            mu = std::sqrt(detG);
-            if (!(mu > 0.0) || !std::isfinite(mu)) return ERR_DEGENERATE;
-            if (formulation == 0) {
-                const double Gi[2][2] = {{G[1][1] / detG, -G[0][1] / detG},
-                                         {-G[1][0] / detG, G[0][0] / detG}};
-                for (int a = 0; a < n; ++a) {
-                    double s[2];
-                    for (int m = 0; m < 2; ++m)
-                        s[m] = Gi[m][0] * R.grad[q][a][0] + Gi[m][1] * R.grad[q][a][1];
-                    for (int c = 0; c < 3; ++c) g[a][c] = J[c][0] * s[0] + J[c][1] * s[1];
-                }
-            } else {
-                double L[3][3], Li[3][3], dummy;
-                const double nrm[3] = {J[1][0] * J[2][1] - J[2][0] * J[1][1],
-                                       J[2][0] * J[0][1] - J[0][0] * J[2][1],
-                                       J[0][0] * J[1][1] - J[1][0] * J[0][1]};
-                for (int c = 0; c < 3; ++c) { L[c][0] = J[c][0]; L[c][1] = J[c][1]; L[c][2] = nrm[c]; }
-                if (!inv3(L, Li, &dummy)) return ERR_DEGENERATE;
-                for (int a = 0; a < n; ++a)
-                    for (int c = 0; c < 3; ++c)  // (L^{-T} v)_c = sum_k Li[k][c] v_k
-                        g[a][c] = Li[0][c] * R.grad[q][a][0] + Li[1][c] * R.grad[q][a][1];
-            }
-        } else {
-            double Ji[3][3], det;
-            if (!inv3(J, Ji, &det)) return ERR_DEGENERATE;
-            mu = std::fabs(det);
-            if (!(mu > 0.0) || !std::isfinite(mu)) return ERR_DEGENERATE;
-            for (int a = 0; a < n; ++a)
-                for (int c = 0; c < 3; ++c)  // (J^{-T} v)_c = sum_k Ji[k][c] v_k
-                    g[a][c] = Ji[0][c] * R.grad[q][a][0] + Ji[1][c] * R.grad[q][a][1] +
-                              Ji[2][c] * R.grad[q][a][2];
-        }
+        const int st = point_gradients(R, J, q, formulation, &mu, g);
+        if (st != OK) return st;
         double aq = 1.0;
         if (u) {
             double uq = 0.0;
@@ -311,6 +339,46 @@ int element_matrices(const Ref& R, const double* X /* nref x 3 */, const double*
                 Al[a * n + b] += w * mu * gg;
                 Aal[a * n + b] += w * mu * aq * gg;
             }
+    }
+    return OK;
+}
+
+enum { RHS_LOAD = 1, RHS_KLL = 2 };
+
+int rhs_ncomp(int kind) { return kind == RHS_LOAD ? 1 : 4; }
+
+// Local right-hand side of one element (nref x ncomp, row-major [a][k]).
+//   RHS_LOAD: U = f (nref x 1):  F[a] = sum_q w mu f_h(xi_q) phi_a(xi_q)
+//   RHS_KLL:  U = (nu_1, nu_2, nu_3, H) (nref x 4):
+//             alpha^2 = sum_k |sum_c U[c][k] g_c|^2            (Listing 2 l.2)
+//             F[a][k] = sum_q w mu alpha^2 u_{h,k} phi_a       (Listing 2 l.3-4)
+int element_rhs(const Ref& R, const double* X, const double* U, int kind, int formulation, double* F) {
+    const int n = R.nref, nc = rhs_ncomp(kind);
+    for (int i = 0; i < n * nc; ++i) F[i] = 0.0;
+    for (size_t q = 0; q < R.rule.size(); ++q) {
+        const double w = R.rule[q].w;
+        double J[3][3];
+        jacobian(R, X, q, J);
+        double mu = 0.0;
+        double g[10][3];
+        const int st = point_gradients(R, J, q, formulation, &mu, g);
+        if (st != OK) return st;
+        double uq[4] = {0.0, 0.0, 0.0, 0.0};  // u_h(xi_q), per component
+        for (int k = 0; k < nc; ++k)
+            for (int c = 0; c < n; ++c) uq[k] += U[c * nc + k] * R.phi[q][c];
+        double weight = w * mu;
+        if (kind == RHS_KLL) {
+            double alpha2 = 0.0;
+            for (int k = 0; k < 3; ++k) {
+                double grad_nu_k[3] = {0.0, 0.0, 0.0};  // grad_Gamma_h of component k of nu_h
+                for (int c = 0; c < n; ++c)
+                    for (int i = 0; i < 3; ++i) grad_nu_k[i] += U[c * nc + k] * g[c][i];
+                for (int i = 0; i < 3; ++i) alpha2 += grad_nu_k[i] * grad_nu_k[i];
+            }
+            weight *= alpha2;
+        }
+        for (int a = 0; a < n; ++a)
+            for (int k = 0; k < nc; ++k) F[a * nc + k] += weight * uq[k] * R.phi[q][a];
     }
     return OK;
 }
@@ -510,6 +578,103 @@ int oracle_assemble_rows(int domain, int order, int quad, int64_t n_nodes, const
         for (int k = 0; k < 3; ++k) std::free(P.vals[k]);
     }
     return OK;
+}
+
+// Local right-hand side of one element: U is nref x ncomp (row-major), F likewise.
+int oracle_element_rhs(int domain, int order, int quad, const double* X, const double* U, int kind,
+                       int formulation, double* F) {
+    Ref R;
+    if (!make_ref(domain, order, quad, R)) return ERR_UNSUPPORTED;
+    if (kind != RHS_LOAD && kind != RHS_KLL) return ERR_INVALID_ARG;
+    if ((kind == RHS_KLL || formulation == 1) && domain != SURFACE_TRI) return ERR_UNSUPPORTED;
+    return element_rhs(R, X, U, kind, formulation, F);
+}
+
+// Assemble the right-hand side `kind` into the rows `rows` (ascending,
+// unique).  u: ncomp x n_nodes, component-major (u[k * n_nodes + c], the
+// paper's index j + (k-1) N); out (and out_abs, if not null): ncomp x
+// n_rows, component-major.  out_abs accumulates |local entries| (the scale of
+// the rounding error, used by the parity tolerance).  Per row: ascending
+// element id.
+int oracle_assemble_rhs_rows(int domain, int order, int quad, int64_t n_nodes, const double* coords,
+                             int64_t n_elems, const int32_t* conn, const double* u, int kind, int64_t n_rows,
+                             const int64_t* rows, int nthreads, double* out, double* out_abs, int64_t* bad_elem) {
+    *bad_elem = -1;
+    Ref R;
+    if (!make_ref(domain, order, quad, R)) return ERR_UNSUPPORTED;
+    if (kind != RHS_LOAD && kind != RHS_KLL) return ERR_INVALID_ARG;
+    if (kind == RHS_KLL && domain != SURFACE_TRI) return ERR_UNSUPPORTED;
+    if (!u || !out) return ERR_INVALID_ARG;
+    const int n = R.nref, nc = rhs_ncomp(kind);
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (int a = 0; a < n; ++a) {
+            const int32_t v = conn[e * n + a];
+            if (v < 0 || v >= n_nodes) { *bad_elem = e; return ERR_INDEX; }
+        }
+    for (int64_t i = 0; i < n_rows; ++i)
+        if (rows[i] < 0 || rows[i] >= n_nodes || (i > 0 && rows[i] <= rows[i - 1])) return ERR_INVALID_ARG;
+    for (int64_t i = 0; i < nc * n_rows; ++i) {
+        out[i] = 0.0;
+        if (out_abs) out_abs[i] = 0.0;
+    }
+    std::vector<int64_t> inc_ptr(n_nodes + 1, 0);
+    for (int64_t e = 0; e < n_elems; ++e)
+        for (int a = 0; a < n; ++a) inc_ptr[conn[e * n + a] + 1]++;
+    for (int64_t i = 0; i < n_nodes; ++i) inc_ptr[i + 1] += inc_ptr[i];
+    std::vector<int64_t> inc(inc_ptr[n_nodes]);
+    {
+        std::vector<int64_t> cur(inc_ptr.begin(), inc_ptr.end() - 1);
+        for (int64_t e = 0; e < n_elems; ++e)
+            for (int a = 0; a < n; ++a) inc[cur[conn[e * n + a]]++] = e;
+    }
+    if (nthreads < 1) nthreads = 1;
+    int64_t BLOCK = (n_rows + 4 * nthreads - 1) / (4 * (int64_t)nthreads);
+    if (BLOCK < 1024) BLOCK = 1024;
+    if (BLOCK > (1 << 18)) BLOCK = 1 << 18;
+    const int64_t nblocks = (n_rows + BLOCK - 1) / BLOCK;
+    std::vector<int64_t> bad(nblocks, -1);
+    auto run_block = [&](int64_t b) {
+        const int64_t r0 = b * BLOCK, r1 = std::min(n_rows, r0 + BLOCK);
+        std::vector<int64_t> elems;
+        for (int64_t i = r0; i < r1; ++i)
+            for (int64_t k = inc_ptr[rows[i]]; k < inc_ptr[rows[i] + 1]; ++k) elems.push_back(inc[k]);
+        std::sort(elems.begin(), elems.end());
+        elems.erase(std::unique(elems.begin(), elems.end()), elems.end());
+        std::vector<double> X(3 * n), U(n * nc), F(n * nc);
+        for (int64_t e : elems) {
+            for (int a = 0; a < n; ++a) {
+                const int32_t v = conn[e * n + a];
+                for (int c = 0; c < 3; ++c) X[3 * a + c] = coords[3 * (int64_t)v + c];
+                for (int k = 0; k < nc; ++k) U[a * nc + k] = u[k * n_nodes + v];
+            }
+            if (element_rhs(R, X.data(), U.data(), kind, 0, F.data()) != OK) {
+                if (bad[b] < 0 || e < bad[b]) bad[b] = e;
+                continue;
+            }
+            for (int a = 0; a < n; ++a) {
+                const int64_t row = conn[e * n + a];
+                const int64_t* it = std::lower_bound(rows + r0, rows + r1, row);
+                if (it == rows + r1 || *it != row) continue;
+                const int64_t i = it - rows;
+                for (int k = 0; k < nc; ++k) {
+                    out[k * n_rows + i] += F[a * nc + k];
+                    if (out_abs) out_abs[k * n_rows + i] += std::fabs(F[a * nc + k]);
+                }
+            }
+        }
+    };
+    {
+        std::vector<std::thread> pool;
+        const int T = (int)std::min<int64_t>(nthreads, std::max<int64_t>(1, nblocks));
+        for (int t = 0; t < T; ++t)
+            pool.emplace_back([&, t]() {
+                for (int64_t b = t; b < nblocks; b += T) run_block(b);
+            });
+        for (auto& th : pool) th.join();
+    }
+    for (int64_t b = 0; b < nblocks; ++b)
+        if (bad[b] >= 0 && (*bad_elem < 0 || bad[b] < *bad_elem)) *bad_elem = bad[b];
+    return *bad_elem >= 0 ? ERR_DEGENERATE : OK;
 }
 
 }  // extern "C"

@@ -20,6 +20,9 @@ _LIB = None
 
 K_MASS, K_STIFF, K_STIFF_COEF = 1, 2, 4
 KIND_BITS = {"M": K_MASS, "A": K_STIFF, "Aa": K_STIFF_COEF}
+RHS_LOAD, RHS_KLL = 1, 2
+RHS_KINDS = {"load": RHS_LOAD, "kll": RHS_KLL}
+RHS_NCOMP = {RHS_LOAD: 1, RHS_KLL: 4}
 
 
 class OracleError(RuntimeError):
@@ -59,6 +62,11 @@ def lib():
         L.oracle_element.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int, vp, vp, vp]
         L.oracle_rule.argtypes = [ctypes.c_int, vp, vp, vp]
         L.oracle_basis.argtypes = [ctypes.c_int, ctypes.c_int, vp, vp, vp]
+        L.oracle_element_rhs.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int,
+                                         ctypes.c_int, vp]
+        L.oracle_assemble_rhs_rows.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp,
+                                               ctypes.c_int64, vp, vp, ctypes.c_int, ctypes.c_int64, vp,
+                                               ctypes.c_int, vp, vp, ctypes.POINTER(ctypes.c_int64)]
         _LIB = L
     return _LIB
 
@@ -129,6 +137,52 @@ def element_matrices(domain: int, order: int, quad: int, X, u=None, formulation:
     if st != 0:
         raise OracleError(st)
     return M, A, Aa
+
+
+def _rhs_kind(kind) -> int:
+    return RHS_KINDS[kind] if isinstance(kind, str) else int(kind)
+
+
+def element_rhs(domain: int, order: int, quad: int, X, U, kind="load", formulation: int = 0) -> np.ndarray:
+    """Local right-hand side (nref x ncomp) of one element; U is nref x ncomp nodal data
+    (load: f; kll: (nu_1, nu_2, nu_3, H))."""
+    L = lib()
+    k = _rhs_kind(kind)
+    X = np.ascontiguousarray(X, dtype=np.float64)
+    n = X.shape[0]
+    nc = RHS_NCOMP.get(k, 1)
+    U = np.ascontiguousarray(np.asarray(U, dtype=np.float64).reshape(n, nc))
+    F = np.zeros((n, nc))
+    st = L.oracle_element_rhs(domain, order, quad, _p(X), _p(U), k, formulation, _p(F))
+    if st != 0:
+        raise OracleError(st)
+    return F
+
+
+def assemble_rhs_rows(mesh, u, kind="load", rows=None, nthreads: Optional[int] = None,
+                      with_abs: bool = False):
+    """Oracle right-hand side of the given global rows (default all): returns an
+    (ncomp, n_rows) array (and the matching sum of |local entries| if with_abs).
+    u: (ncomp, n_nodes) nodal data, component-major."""
+    L = lib()
+    k = _rhs_kind(kind)
+    nc = RHS_NCOMP.get(k, 1)
+    if rows is None:
+        rows = np.arange(mesh.n_nodes, dtype=np.int64)
+    rows = np.ascontiguousarray(rows, dtype=np.int64)
+    coords = np.ascontiguousarray(mesh.coords, dtype=np.float64)
+    conn = np.ascontiguousarray(mesh.conn, dtype=np.int32)
+    uu = np.ascontiguousarray(np.asarray(u, dtype=np.float64).reshape(nc, mesh.n_nodes))
+    out = np.zeros((nc, rows.size))
+    oabs = np.zeros((nc, rows.size)) if with_abs else None
+    bad = ctypes.c_int64(-1)
+    nt = nthreads or (os.cpu_count() or 1)
+    st = L.oracle_assemble_rhs_rows(mesh.domain, mesh.order, mesh.quad, mesh.n_nodes, _p(coords),
+                                    mesh.n_elems, _p(conn), _p(uu), k, rows.size, _p(rows), nt,
+                                    _p(out), _p(oabs), ctypes.byref(bad))
+    if st != 0:
+        raise OracleError(st, bad.value)
+    return (out, oabs) if with_abs else out
 
 
 def rule(quad: int):
