@@ -166,6 +166,36 @@ lfem_status lfem_assemble_numeric_host(lfem_plan p, unsigned kinds, const double
                                        const double* coeff_h, double* const vals_h[3],
                                        lfem_stream_t stream);
 
+/* Right-hand sides, assembled into the plan's owned
+ * rows with the same deterministic order as the matrices (per row: ascending
+ * element id; no atomics).
+ *   LFEM_RHS_LOAD (all families; 1 input / 1 output component):
+ *       b_j = sum_E sum_q w_q mu_E(xi_q) f_h(xi_q) phi_j(xi_q),  f_h = sum_c f_c phi_c
+ *       (PAPER.md Eq. "load vector" P:168-177; equals M f with the element rule).
+ *   LFEM_RHS_KLL (surface triangles only; 4 input / 4 output components):
+ *       u = (nu_1, nu_2, nu_3, H) nodal,
+ *       alpha^2 = |grad_{Gamma_h} nu_h|^2 (Frobenius; Listing 2 line 2),
+ *       f_{k,j} = sum_E sum_q w_q mu alpha^2 u_{h,k}(xi_q) phi_j(xi_q), k = 1..4
+ *       (f_1 = first three components, f_2 = the H component; P:784-789,
+ *       Listing 2 lines 3-4).
+ * Layout: u is ncomp x n_nodes, component-major (u[k * n_nodes + node], the
+ * paper's index j + (k-1) N), device, BORROWED; out is ncomp x n_rows,
+ * component-major over the owned rows (out[k * n_rows + (row - row_begin)]),
+ * device, CALLER-OWNED.  coords: device n_nodes x 3 (moving geometry) or NULL
+ * for the mesh's coordinates.  The first call per plan builds the row
+ * incidence lists and a plan-owned staging buffer (n_elems_local * nref *
+ * ncomp fp64) and synchronises `stream`; later calls only enqueue (two
+ * kernels).  Errors: INVALID_ARG (NULL u/out, unknown kind), UNSUPPORTED (KLL
+ * on a bulk mesh); degenerate elements are latched as for the matrices
+ * (lfem_plan_check). */
+typedef enum { LFEM_RHS_LOAD = 1, LFEM_RHS_KLL = 2 } lfem_rhs_kind;
+lfem_status lfem_assemble_rhs(lfem_plan p, int kind, const double* coords, const double* u, double* out,
+                              lfem_stream_t stream);
+/* Components of a right-hand side kind (1 or 4), 0 if unknown. */
+int lfem_rhs_ncomp(int kind);
+/* Kernel launches lfem_assemble_rhs enqueues once the plan's incidence lists exist. */
+int lfem_rhs_launches(lfem_plan p, int kind);
+
 /* CSR pattern of the plan: device pointers, PLAN-OWNED.
  * row_ptr: n_rows + 1 int64 (relative to the block); col_idx: nnz int32 (global). */
 lfem_status lfem_csr_get(lfem_plan p, const int64_t** row_ptr, const int32_t** col_idx);

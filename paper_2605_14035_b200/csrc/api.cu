@@ -86,6 +86,9 @@ void free_plan_memory(lfem_plan_s* p) {
     dev_free(p->d_coords, s);
     dev_free(p->d_coeff, s);
     for (int k = 0; k < 3; ++k) dev_free(p->d_vals[k], s);
+    dev_free(p->rhs_ptr, s);
+    dev_free(p->rhs_codes, s);
+    dev_free(p->rhs_stage, s);
     free_tiles(p->tiles, s);
     delete p->prof;
     p->prof = nullptr;
@@ -377,6 +380,26 @@ lfem_status lfem_spmv(lfem_plan p, const double* vals, const double* x_full, dou
     if ((p->nnz > 0 && !vals) || (p->n_rows > 0 && (!x_full || !y_rows)))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL vector");
     return spmv_launch(p, vals, x_full, y_rows, S(stream));
+}
+
+int lfem_rhs_ncomp(int kind) { return kind == LFEM_RHS_LOAD ? 1 : kind == LFEM_RHS_KLL ? 4 : 0; }
+
+int lfem_rhs_launches(lfem_plan p, int kind) {
+    if (!p || lfem_rhs_ncomp(kind) == 0) return 0;
+    return (p->n_local > 0 ? 1 : 0) + (p->n_rows > 0 ? 1 : 0);
+}
+
+lfem_status lfem_assemble_rhs(lfem_plan p, int kind, const double* coords, const double* u, double* out,
+                              lfem_stream_t stream) {
+    g_err.clear();
+    g_err_elem = -1;
+    if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
+    if (lfem_rhs_ncomp(kind) == 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "kind must be LFEM_RHS_LOAD or LFEM_RHS_KLL");
+    if (kind == LFEM_RHS_KLL && p->mesh->domain != LFEM_SURFACE_TRI)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "the KLL right-hand side is defined on surfaces only");
+    if (!u && p->mesh->n_nodes > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "u is NULL");
+    if (!out && p->n_rows > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "out is NULL");
+    return rhs_dispatch(p, kind, coords ? coords : p->mesh->coords, u, out, S(stream));
 }
 
 lfem_status lfem_plan_check(lfem_plan p, lfem_stream_t stream) {

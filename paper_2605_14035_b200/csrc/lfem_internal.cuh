@@ -75,6 +75,10 @@ struct lfem_plan_s {
     double* d_coords = nullptr;
     double* d_coeff = nullptr;
     double* d_vals[3] = {nullptr, nullptr, nullptr};
+    // right-hand sides (rhs.cuh): per owned row, its incident (element, a) in ascending element order
+    int64_t* rhs_ptr = nullptr;     // n_rows + 1
+    int32_t* rhs_codes = nullptr;   // le * nref + a
+    double* rhs_stage = nullptr;    // n_local x nref x 4
 };
 
 // ---------------------------------------------------------------------------
@@ -143,6 +147,8 @@ void free_tiles(TilePlan& t, cudaStream_t s);
 lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
                              double* const vals[3], cudaStream_t s);
 int numeric_launch_count(lfem_plan_s* p, unsigned kinds);
+lfem_status rhs_dispatch(lfem_plan_s* p, int kind, const double* coords, const double* u, double* out,
+                         cudaStream_t s);
 lfem_status spmv_launch(lfem_plan_s* p, const double* vals, const double* x, double* y, cudaStream_t s);
 lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const double* b, double* out,
                          cudaStream_t s);

@@ -333,3 +333,5 @@ lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const
     LFEM_CUDA(cudaGetLastError());
     return LFEM_OK;
 }
+
+#include "rhs.cuh"

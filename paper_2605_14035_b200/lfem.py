@@ -25,6 +25,8 @@ LFEM_SURFACE_TRI, LFEM_BULK_TET = 0, 1
 LFEM_QUAD_DEFAULT, LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4, LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4 = range(5)
 LFEM_MASS, LFEM_STIFF, LFEM_STIFF_COEF = 1, 2, 4
 LFEM_NUMERIC_AUTO, LFEM_NUMERIC_V0, LFEM_NUMERIC_TILED = 0, 1, 2
+LFEM_RHS_LOAD, LFEM_RHS_KLL = 1, 2
+RHS_KINDS = {"load": LFEM_RHS_LOAD, "kll": LFEM_RHS_KLL}
 KIND_BITS = {"M": LFEM_MASS, "A": LFEM_STIFF, "Aa": LFEM_STIFF_COEF}
 KIND_INDEX = {"M": 0, "A": 1, "Aa": 2}
 
@@ -33,7 +35,8 @@ EXPORTED = ("lfem_mesh_create", "lfem_mesh_destroy", "lfem_assemble_symbolic", "
             "lfem_plan_info", "lfem_plan_set_variant", "lfem_assemble_numeric", "lfem_assemble_numeric_coords",
             "lfem_assemble_numeric_host", "lfem_csr_get", "lfem_spmv", "lfem_plan_check", "lfem_axpby",
             "lfem_numeric_launches", "lfem_error_element", "lfem_last_error", "lfem_version",
-            "lfem_profile_enable", "lfem_profile_read", "lfem_set_allocator")
+            "lfem_profile_enable", "lfem_profile_read", "lfem_set_allocator", "lfem_assemble_rhs",
+            "lfem_rhs_ncomp", "lfem_rhs_launches")
 
 
 class LfemError(RuntimeError):
@@ -78,6 +81,9 @@ def _lib():
         L.lfem_last_error.restype = ctypes.c_char_p
         L.lfem_version.restype = ctypes.c_char_p
         L.lfem_set_allocator.argtypes = [vp, vp, vp]
+        L.lfem_assemble_rhs.argtypes = [vp, c_int, vp, vp, vp, vp]
+        L.lfem_rhs_ncomp.argtypes = [c_int]
+        L.lfem_rhs_launches.argtypes = [vp, c_int]
         _LIB = L
     return _LIB
 
@@ -228,6 +234,22 @@ def lfem_spmv(plan: Plan, vals: torch.Tensor, x_full: torch.Tensor, y_rows: torc
     _check(_lib().lfem_spmv(plan.handle, _dptr(vals), _dptr(x_full), _dptr(y_rows), _stream(stream)), "lfem_spmv")
 
 
+def lfem_rhs_ncomp(kind: int) -> int:
+    return int(_lib().lfem_rhs_ncomp(kind))
+
+
+def lfem_rhs_launches(plan: Plan, kind: int) -> int:
+    return int(_lib().lfem_rhs_launches(plan.handle, kind))
+
+
+def lfem_assemble_rhs(plan: Plan, kind: int, coords: Optional[torch.Tensor], u: torch.Tensor, out: torch.Tensor,
+                      stream=None):
+    """Right-hand side `kind` (LFEM_RHS_LOAD / LFEM_RHS_KLL): u is (ncomp, n_nodes) fp64 on the device,
+    out (ncomp, n_rows) fp64 on the device (component-major); coords None = the mesh's."""
+    st = _lib().lfem_assemble_rhs(plan.handle, kind, _dptr(coords), _dptr(u), _dptr(out), _stream(stream))
+    _check(st, "lfem_assemble_rhs")
+
+
 def lfem_plan_check(plan: Plan, stream=None):
     _check(_lib().lfem_plan_check(plan.handle, _stream(stream)), "lfem_plan_check")
 
@@ -316,3 +338,21 @@ def assemble(mesh_arrays, kinds=("M", "A"), coeff=None, row_begin=0, row_end=Non
     row_ptr, col_idx = lfem_csr_get(plan)
     plan._keep = (coords, conn, cf)
     return plan, row_ptr, col_idx, {k: vals[KIND_INDEX[k]] for k in kinds}
+
+
+def assemble_rhs(mesh_arrays, u, kind="load", row_begin=0, row_end=None, device="cuda", plan=None):
+    """Upload a lfem_inputs.Mesh-like object and nodal data u ((ncomp, n_nodes), component-major),
+    run symbolic (unless `plan` is given) + the right-hand side; returns (plan, out (ncomp, n_rows))."""
+    k = RHS_KINDS[kind] if isinstance(kind, str) else int(kind)
+    nc = lfem_rhs_ncomp(k)
+    if plan is None:
+        coords = torch.as_tensor(mesh_arrays.coords, device=device).contiguous()
+        conn = torch.as_tensor(mesh_arrays.conn, device=device).contiguous()
+        m = lfem_mesh_create(mesh_arrays.domain, mesh_arrays.order, mesh_arrays.quad, coords, conn)
+        plan = lfem_assemble_symbolic(m, row_begin, row_end)
+        plan._keep = (coords, conn)
+    uu = torch.as_tensor(u, dtype=torch.float64, device=device).reshape(nc, -1).contiguous()
+    out = torch.empty((nc, plan.n_rows), dtype=torch.float64, device=device)
+    lfem_assemble_rhs(plan, k, None, uu, out)
+    lfem_plan_check(plan)
+    return plan, out
