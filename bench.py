@@ -118,20 +118,23 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) legs
-def _oracle_rows_for(m, kinds, coeff, target_s, nt):
+def _oracle_rows_for(m, kinds, coeff, target_s, nt, call=None):
     """Rows of a contiguous block that take about target_s seconds in the oracle.
     The oracle has a per-call setup (node -> element incidence over the whole
     mesh) and a per-row cost: a tiny sample measures the first, a 5 % sample the
     second; the per-row cost grows with the sample (map sizes, caches), hence a
     safety factor of 1.7 (measured on C5 at level 8: 0.8 us/row at 2 %, 1.35 at 100 %)."""
     import oracle
+    if call is None:
+        def call(rows):
+            oracle.assemble_rows(m, kinds, rows=rows, coeff=coeff, nthreads=nt)
     r0 = min(m.n_nodes, 100)
     r1 = min(m.n_nodes, max(50000, m.n_nodes // 20))
     t0 = time.perf_counter()
-    oracle.assemble_rows(m, kinds, rows=np.arange(r0, dtype=np.int64), coeff=coeff, nthreads=nt)
+    call(np.arange(r0, dtype=np.int64))
     setup = time.perf_counter() - t0
     t0 = time.perf_counter()
-    oracle.assemble_rows(m, kinds, rows=np.arange(r1, dtype=np.int64), coeff=coeff, nthreads=nt)
+    call(np.arange(r1, dtype=np.int64))
     t1 = time.perf_counter() - t0
     per_row = max((t1 - setup) / max(1, r1 - r0), t1 / r1 * 1e-3, 1e-9)
     rows = int(r0 + max(0.0, target_s - setup) / (1.7 * per_row))
@@ -151,10 +154,32 @@ def oracle_sample(m, kinds, coeff, target_s):
     return equiv_elems / dt, rows, dt, nt, c.nnz
 
 
+def rhs_fields(m, kind):
+    """Synthetic nodal data of the right-hand side workloads: load f = a seeded
+    smooth-ish field; KLL u = (nu; H), nu = x/|x| + 0.05 noise (a perturbed unit normal on the
+    sphere), H = 2 + 0.1 noise (the unit sphere's mean curvature, perturbed)."""
+    import lfem_inputs as li
+    if kind == "load":
+        return np.ascontiguousarray(li.random_field(m, 5)[None, :])
+    x = m.coords
+    r = np.sqrt(np.einsum("ij,ij->i", x, x))
+    r[r == 0] = 1.0
+    nu = (x / r[:, None]).T + 0.05 * np.vstack([li.random_field(m, 5 + k) for k in range(3)])
+    H = 2.0 + 0.1 * li.random_field(m, 8)
+    return np.ascontiguousarray(np.vstack([nu, H[None, :]]))
+
+
+def rhs_alg_bytes(n_elems, nref, n_nodes_in, n_rows, nc):
+    """conn + coords (each node once) + nodal input u (ncomp per node) + output (ncomp per owned row)."""
+    return n_elems * nref * 4 + n_nodes_in * 24 + n_nodes_in * nc * 8 + n_rows * nc * 8
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
+    if args.rhs:
+        return run_reference_rhs(args)
     name = args.config
     m, gen_s = build_mesh(name)
     kinds = m.extra["kinds"]
@@ -186,6 +211,194 @@ def run_reference(args):
                                        f"(elements/s = n_elems * rows/n_rows / t); per-step sample"},
             "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_reference_rhs(args):
+    import oracle
+    name, kind = args.config, args.rhs
+    m, _ = build_mesh(name)
+    u = rhs_fields(m, kind)
+    nt = os.cpu_count() or 1
+    budget = float(os.environ.get("LFEM_REF_BUDGET_S", "90"))
+    per_step = budget / max(1, args.steps + args.warmup)
+
+    def call(rows):
+        oracle.assemble_rhs_rows(m, u, kind, rows=rows, nthreads=nt)
+    rows = max(2000, _oracle_rows_for(m, None, None, per_step, nt, call=call))
+    times = []
+    for it in range(args.warmup + args.steps):
+        r0 = (it * rows) % max(1, m.n_nodes - rows + 1)
+        t0 = time.perf_counter()
+        call(np.arange(r0, r0 + rows, dtype=np.int64))
+        if it >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times)
+    value = m.n_elems * rows / m.n_nodes * len(times) / t
+    line = {"impl": "reference", "metric": f"elements/s (fp64 {kind} right-hand side assembly)",
+            "value": value, "unit": "elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t / len(times), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded, lfem_inputs)",
+            "config": {"workload": f"{name} mesh, {kind} right-hand side", "rhs": kind},
+            "cpu_baseline": {"value": value, "unit": "elements/s", "cores": nt, "kind": "oracle",
+                             "sample": f"{rows} contiguous rows per step of {m.n_nodes}"},
+            "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg: right-hand sides
+def run_rhs(args):
+    """One step = one lfem_assemble_rhs call over the config's mesh; 1 GPU
+    or row blocks over ranks like the matrices (no collective)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2605_14035_b200 import lfem
+    from paper_2605_14035_b200.partition import partition_rows
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("LFEM_BENCH_DEVICE") is not None:
+        local = int(os.environ["LFEM_BENCH_DEVICE"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        backend = os.environ.get("LFEM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+    name, kind = args.config, args.rhs
+    k = lfem.RHS_KINDS[kind]
+    nc = lfem.lfem_rhs_ncomp(k)
+    m, gen_s = build_mesh(name)  # every rank generates the same seeded mesh (no broadcast needed)
+    u_np = rhs_fields(m, kind)
+    coords = torch.as_tensor(m.coords).to(dev)
+    conn = torch.as_tensor(m.conn).to(dev)
+    u = torch.as_tensor(u_np).to(dev)
+    bounds = partition_rows(m.conn, m.n_nodes, world) if world > 1 else [0, m.n_nodes]
+    r0, r1 = bounds[rank], bounds[rank + 1]
+    stream = torch.cuda.current_stream()
+    mesh = lfem.lfem_mesh_create(m.domain, m.order, m.quad, coords, conn)
+    plan = lfem.lfem_assemble_symbolic(mesh, r0, r1)
+    out = torch.empty((nc, plan.n_rows), dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    lfem.lfem_assemble_rhs(plan, k, None, u, out)  # first call builds the row incidence lists
+    torch.cuda.synchronize()
+    first_ms = 1e3 * (time.perf_counter() - t0)
+    for _ in range(1, args.warmup):
+        lfem.lfem_assemble_rhs(plan, k, None, u, out)
+    lfem.lfem_plan_check(plan)
+    alg = rhs_alg_bytes(plan.n_elems_local, m.nref, m.n_nodes, plan.n_rows, nc)
+    flush = alg < 4 * L2_BYTES
+    flush_buf = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for t in range(args.steps):
+        if flush:
+            flush_buf.zero_()
+        ev[t][0].record(stream)
+        lfem.lfem_assemble_rhs(plan, k, None, u, out)
+        ev[t][1].record(stream)
+    torch.cuda.synchronize()
+    elapsed_ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        dist.barrier()
+    lfem.lfem_plan_check(plan)
+    lfem.lfem_profile_enable(plan, True)
+    nprof = max(3, min(args.steps, 20))
+    for _ in range(nprof):
+        if flush:
+            flush_buf.zero_()
+        lfem.lfem_assemble_rhs(plan, k, None, u, out)
+    prof = lfem.lfem_profile_read(plan)
+    lfem.lfem_profile_enable(plan, False)
+    clk = clocks.stop()
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tmax)
+    ms_per_step = elapsed_ms / args.steps
+    value = m.n_elems * args.steps / (elapsed_ms * 1e-3)
+
+    # e2e through the public API: pinned host coords + u -> device, lfem_assemble_rhs, device -> pinned host
+    e2e = None
+    if not args.no_e2e:
+        coords_h = torch.as_tensor(m.coords).pin_memory()
+        u_h = torch.as_tensor(u_np).pin_memory()
+        out_h = torch.empty((nc, plan.n_rows), dtype=torch.float64, pin_memory=True)
+        c_d, u_d = torch.empty_like(coords), torch.empty_like(u)
+        ke = max(1, min(args.steps, args.e2e_steps))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            c_d.copy_(coords_h, non_blocking=True)
+            u_d.copy_(u_h, non_blocking=True)
+            lfem.lfem_assemble_rhs(plan, k, c_d, u_d, out)
+            out_h.copy_(out, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        assert torch.equal(out_h, out.cpu()), "e2e result differs from the device path"
+        e2e = {"value": m.n_elems * ke / (float(te) * 1e-3), "unit": "elements/s",
+               "h2d_bytes_per_step": int((coords_h.numel() + u_h.numel()) * 8 * world),
+               "d2h_bytes_per_step": int(m.n_nodes * nc * 8), "api": "lfem_assemble_rhs (+ pinned H2D/D2H copies)",
+               "steps": ke}
+
+    hbm, peak_src = peaks()
+    step_kernel_ms = sum(v[0] for v in prof.values()) / max(1, nprof)
+    achieved = alg / (step_kernel_ms * 1e-3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp))
+        tr = [tj.get(f"{name}-{kind}:{kn}") for kn in prof]
+        traffic = sum(tr) if tr and all(x is not None for x in tr) else None
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": traffic, "kernel": "+".join(prof), "algorithmic_bytes_per_launch": int(alg),
+                "kernel_ms": step_kernel_ms, "peak_source": peak_src,
+                "per_kernel_ms": {kn: v[0] / max(1, v[1]) for kn, v in prof.items()},
+                "note": "algorithmic bytes of the whole step (two kernels); traffic = their ncu DRAM sum"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        nt = os.cpu_count() or 1
+
+        def call(rows):
+            oracle.assemble_rhs_rows(m, u_np, kind, rows=rows, nthreads=nt)
+        rows = _oracle_rows_for(m, None, None, args.cpu_seconds, nt, call=call)
+        t0 = time.perf_counter()
+        call(np.arange(rows, dtype=np.int64))
+        dt = time.perf_counter() - t0
+        cpu = {"value": m.n_elems * rows / m.n_nodes / dt, "unit": "elements/s", "cores": nt, "kind": "oracle",
+               "sample": f"rows [0, {rows}) of {m.n_nodes} ({dt:.1f} s); elements/s = n_elems * rows/n_rows / t"}
+    if rank == 0:
+        line = {"metric": f"elements/s (fp64 {kind} right-hand side assembly)", "value": value,
+                "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
+                "config": {"workload": f"{name} mesh ({m.n_elems} elements, {m.n_nodes} nodes), {kind} right-hand "
+                                       f"side ({nc} components)", "rhs": kind, "parallelism": f"row-blocks x{world}",
+                           "l2": "flushed (256 MiB write) between steps" if flush else
+                                 "inputs+outputs > L2 (126 MB); no flush"},
+                "first_call_ms": first_ms, "generate_s": gen_s,
+                "gpu_launches": lfem.lfem_rhs_launches(plan, k) * args.steps,
+                "roofline": roofline, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
     return 0
 
 
@@ -489,12 +702,16 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--rhs", default=None, choices=["load", "kll"],
+                    help="time the right-hand side (SURVEY §8(f) N1) instead of the matrices")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.rhs:
+        return run_rhs(args)
     return run_lfem(args)
 
 

@@ -29,8 +29,12 @@ constexpr int RHS_THREADS = 128;
 
 template <int KIND> struct RhsInfo { static constexpr int NC = KIND == LFEM_RHS_KLL ? 4 : 1; };
 
+#ifndef LFEM_RHS_MINB
+#define LFEM_RHS_MINB 1
+#endif
+
 template <int F, int KIND>
-__global__ void __launch_bounds__(RHS_THREADS)
+__global__ void __launch_bounds__(RHS_THREADS, LFEM_RHS_MINB)
 k_rhs_elem(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __restrict__ elem_list,
            const double* __restrict__ coords, const double* __restrict__ u, int64_t n_nodes,
            double* __restrict__ stage, int* __restrict__ err) {
