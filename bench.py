@@ -283,6 +283,8 @@ def run_rhs(args):
     stream = torch.cuda.current_stream()
     mesh = lfem.lfem_mesh_create(m.domain, m.order, m.quad, coords, conn)
     plan = lfem.lfem_assemble_symbolic(mesh, r0, r1)
+    lfem.lfem_plan_set_variant(plan, {"auto": lfem.LFEM_NUMERIC_AUTO, "v0": lfem.LFEM_NUMERIC_V0,
+                                      "tiled": lfem.LFEM_NUMERIC_TILED}[args.variant])
     out = torch.empty((nc, plan.n_rows), dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -390,6 +392,7 @@ def run_rhs(args):
                 "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
                 "config": {"workload": f"{name} mesh ({m.n_elems} elements, {m.n_nodes} nodes), {kind} right-hand "
                                        f"side ({nc} components)", "rhs": kind, "parallelism": f"row-blocks x{world}",
+                           "variant": args.variant,
                            "l2": "flushed (256 MiB write) between steps" if flush else
                                  "inputs+outputs > L2 (126 MB); no flush"},
                 "first_call_ms": first_ms, "generate_s": gen_s,

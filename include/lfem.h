@@ -182,18 +182,22 @@ lfem_status lfem_assemble_numeric_host(lfem_plan p, unsigned kinds, const double
  * paper's index j + (k-1) N), device, BORROWED; out is ncomp x n_rows,
  * component-major over the owned rows (out[k * n_rows + (row - row_begin)]),
  * device, CALLER-OWNED.  coords: device n_nodes x 3 (moving geometry) or NULL
- * for the mesh's coordinates.  The first call per plan builds the row
- * incidence lists and a plan-owned staging buffer (n_elems_local * nref *
- * ncomp fp64) and synchronises `stream`; later calls only enqueue (two
- * kernels).  Errors: INVALID_ARG (NULL u/out, unknown kind), UNSUPPORTED (KLL
- * on a bulk mesh); degenerate elements are latched as for the matrices
+ * for the mesh's coordinates.  The first call per plan (and variant) builds
+ * plan-owned row incidence lists and synchronises `stream`; later calls only
+ * enqueue.  Variants (lfem_plan_set_variant): AUTO / V0 = element kernel +
+ * row reduce through a plan-owned staging buffer (n_elems_local * nref * 4
+ * fp64); TILED = one fused kernel on the matrices' row tiles (local vectors
+ * staged in shared memory; builds the tile plan if the matrices have not;
+ * falls back to V0 where it does not fit; measured slower).
+ * Both give the same bits.  Errors: INVALID_ARG (NULL u/out, unknown kind), UNSUPPORTED
+ * (KLL on a bulk mesh); degenerate elements are latched as for the matrices
  * (lfem_plan_check). */
 typedef enum { LFEM_RHS_LOAD = 1, LFEM_RHS_KLL = 2 } lfem_rhs_kind;
 lfem_status lfem_assemble_rhs(lfem_plan p, int kind, const double* coords, const double* u, double* out,
                               lfem_stream_t stream);
 /* Components of a right-hand side kind (1 or 4), 0 if unknown. */
 int lfem_rhs_ncomp(int kind);
-/* Kernel launches lfem_assemble_rhs enqueues once the plan's incidence lists exist. */
+/* Kernel launches the plan's last lfem_assemble_rhs call enqueued (1 fused, 2 two-kernel). */
 int lfem_rhs_launches(lfem_plan p, int kind);
 
 /* CSR pattern of the plan: device pointers, PLAN-OWNED.

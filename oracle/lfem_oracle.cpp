@@ -352,9 +352,16 @@ int rhs_ncomp(int kind) { return kind == RHS_LOAD ? 1 : 4; }
 //   RHS_KLL:  U = (nu_1, nu_2, nu_3, H) (nref x 4):
 //             alpha^2 = sum_k |sum_c U[c][k] g_c|^2            (Listing 2 l.2)
 //             F[a][k] = sum_q w mu alpha^2 u_{h,k} phi_a       (Listing 2 l.3-4)
-int element_rhs(const Ref& R, const double* X, const double* U, int kind, int formulation, double* F) {
+// Fabs (optional): the same sums evaluated with every term replaced by its absolute
+// value (|U|, |phi|, |g_c|) -- the scale of the rounding error of any evaluation order
+// (running error bound), used by the parity tolerance (reading G33).
+int element_rhs(const Ref& R, const double* X, const double* U, int kind, int formulation, double* F,
+                double* Fabs = nullptr) {
     const int n = R.nref, nc = rhs_ncomp(kind);
-    for (int i = 0; i < n * nc; ++i) F[i] = 0.0;
+    for (int i = 0; i < n * nc; ++i) {
+        F[i] = 0.0;
+        if (Fabs) Fabs[i] = 0.0;
+    }
     for (size_t q = 0; q < R.rule.size(); ++q) {
         const double w = R.rule[q].w;
         double J[3][3];
@@ -367,18 +374,32 @@ int element_rhs(const Ref& R, const double* X, const double* U, int kind, int fo
         for (int k = 0; k < nc; ++k)
             for (int c = 0; c < n; ++c) uq[k] += U[c * nc + k] * R.phi[q][c];
         double weight = w * mu;
+        double wabs = std::fabs(w) * mu;
         if (kind == RHS_KLL) {
-            double alpha2 = 0.0;
+            double alpha2 = 0.0, alpha2_abs = 0.0;
             for (int k = 0; k < 3; ++k) {
                 double grad_nu_k[3] = {0.0, 0.0, 0.0};  // grad_Gamma_h of component k of nu_h
-                for (int c = 0; c < n; ++c)
+                double bound_k = 0.0;                   // sum_c |nu_ck| |g_c|
+                for (int c = 0; c < n; ++c) {
                     for (int i = 0; i < 3; ++i) grad_nu_k[i] += U[c * nc + k] * g[c][i];
+                    bound_k += std::fabs(U[c * nc + k]) *
+                               std::sqrt(g[c][0] * g[c][0] + g[c][1] * g[c][1] + g[c][2] * g[c][2]);
+                }
                 for (int i = 0; i < 3; ++i) alpha2 += grad_nu_k[i] * grad_nu_k[i];
+                alpha2_abs += bound_k * bound_k;
             }
             weight *= alpha2;
+            wabs *= alpha2_abs;
         }
         for (int a = 0; a < n; ++a)
             for (int k = 0; k < nc; ++k) F[a * nc + k] += weight * uq[k] * R.phi[q][a];
+        if (Fabs) {
+            double uabs[4] = {0.0, 0.0, 0.0, 0.0};
+            for (int k = 0; k < nc; ++k)
+                for (int c = 0; c < n; ++c) uabs[k] += std::fabs(U[c * nc + k] * R.phi[q][c]);
+            for (int a = 0; a < n; ++a)
+                for (int k = 0; k < nc; ++k) Fabs[a * nc + k] += wabs * uabs[k] * std::fabs(R.phi[q][a]);
+        }
     }
     return OK;
 }
@@ -593,9 +614,9 @@ int oracle_element_rhs(int domain, int order, int quad, const double* X, const d
 // Assemble the right-hand side `kind` into the rows `rows` (ascending,
 // unique).  u: ncomp x n_nodes, component-major (u[k * n_nodes + c], the
 // paper's index j + (k-1) N); out (and out_abs, if not null): ncomp x
-// n_rows, component-major.  out_abs accumulates |local entries| (the scale of
-// the rounding error, used by the parity tolerance).  Per row: ascending
-// element id.
+// n_rows, component-major.  out_abs accumulates the absolute-value evaluation of
+// every term (element_rhs's Fabs: the scale of the rounding error of any
+// evaluation order, reading G33).  Per row: ascending element id.
 int oracle_assemble_rhs_rows(int domain, int order, int quad, int64_t n_nodes, const double* coords,
                              int64_t n_elems, const int32_t* conn, const double* u, int kind, int64_t n_rows,
                              const int64_t* rows, int nthreads, double* out, double* out_abs, int64_t* bad_elem) {
@@ -640,14 +661,14 @@ int oracle_assemble_rhs_rows(int domain, int order, int quad, int64_t n_nodes, c
             for (int64_t k = inc_ptr[rows[i]]; k < inc_ptr[rows[i] + 1]; ++k) elems.push_back(inc[k]);
         std::sort(elems.begin(), elems.end());
         elems.erase(std::unique(elems.begin(), elems.end()), elems.end());
-        std::vector<double> X(3 * n), U(n * nc), F(n * nc);
+        std::vector<double> X(3 * n), U(n * nc), F(n * nc), Fa(n * nc);
         for (int64_t e : elems) {
             for (int a = 0; a < n; ++a) {
                 const int32_t v = conn[e * n + a];
                 for (int c = 0; c < 3; ++c) X[3 * a + c] = coords[3 * (int64_t)v + c];
                 for (int k = 0; k < nc; ++k) U[a * nc + k] = u[k * n_nodes + v];
             }
-            if (element_rhs(R, X.data(), U.data(), kind, 0, F.data()) != OK) {
+            if (element_rhs(R, X.data(), U.data(), kind, 0, F.data(), out_abs ? Fa.data() : nullptr) != OK) {
                 if (bad[b] < 0 || e < bad[b]) bad[b] = e;
                 continue;
             }
@@ -658,7 +679,7 @@ int oracle_assemble_rhs_rows(int domain, int order, int quad, int64_t n_nodes, c
                 const int64_t i = it - rows;
                 for (int k = 0; k < nc; ++k) {
                     out[k * n_rows + i] += F[a * nc + k];
-                    if (out_abs) out_abs[k * n_rows + i] += std::fabs(F[a * nc + k]);
+                    if (out_abs) out_abs[k * n_rows + i] += Fa[a * nc + k];
                 }
             }
         }

@@ -89,6 +89,7 @@ void free_plan_memory(lfem_plan_s* p) {
     dev_free(p->rhs_ptr, s);
     dev_free(p->rhs_codes, s);
     dev_free(p->rhs_stage, s);
+    dev_free(p->rhs_tcodes, s);
     free_tiles(p->tiles, s);
     delete p->prof;
     p->prof = nullptr;
@@ -386,7 +387,7 @@ int lfem_rhs_ncomp(int kind) { return kind == LFEM_RHS_LOAD ? 1 : kind == LFEM_R
 
 int lfem_rhs_launches(lfem_plan p, int kind) {
     if (!p || lfem_rhs_ncomp(kind) == 0) return 0;
-    return (p->n_local > 0 ? 1 : 0) + (p->n_rows > 0 ? 1 : 0);
+    return rhs_launch_count(p);
 }
 
 lfem_status lfem_assemble_rhs(lfem_plan p, int kind, const double* coords, const double* u, double* out,

@@ -78,7 +78,11 @@ struct lfem_plan_s {
     // right-hand sides (rhs.cuh): per owned row, its incident (element, a) in ascending element order
     int64_t* rhs_ptr = nullptr;     // n_rows + 1
     int32_t* rhs_codes = nullptr;   // le * nref + a
-    double* rhs_stage = nullptr;    // n_local x nref x 4
+    double* rhs_stage = nullptr;    // n_local x nref x 4 (two-kernel variant)
+    int64_t rhs_total = 0;          // entries of rhs_codes
+    uint16_t* rhs_tcodes = nullptr; // fused variant: e_tile * nref + a, same indexing as rhs_codes
+    int rhs_tiled = -1;             // -1 not tried, 0 unavailable, 1 tile-local codes built
+    int rhs_last_tiled = -1;        // variant of the last lfem_assemble_rhs call (1 fused, 0 two-kernel)
 };
 
 // ---------------------------------------------------------------------------
@@ -149,6 +153,7 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
 int numeric_launch_count(lfem_plan_s* p, unsigned kinds);
 lfem_status rhs_dispatch(lfem_plan_s* p, int kind, const double* coords, const double* u, double* out,
                          cudaStream_t s);
+int rhs_launch_count(lfem_plan_s* p);
 lfem_status spmv_launch(lfem_plan_s* p, const double* vals, const double* x, double* y, cudaStream_t s);
 lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const double* b, double* out,
                          cudaStream_t s);

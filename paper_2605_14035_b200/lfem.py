@@ -340,7 +340,8 @@ def assemble(mesh_arrays, kinds=("M", "A"), coeff=None, row_begin=0, row_end=Non
     return plan, row_ptr, col_idx, {k: vals[KIND_INDEX[k]] for k in kinds}
 
 
-def assemble_rhs(mesh_arrays, u, kind="load", row_begin=0, row_end=None, device="cuda", plan=None):
+def assemble_rhs(mesh_arrays, u, kind="load", row_begin=0, row_end=None, device="cuda", plan=None,
+                 variant=None):
     """Upload a lfem_inputs.Mesh-like object and nodal data u ((ncomp, n_nodes), component-major),
     run symbolic (unless `plan` is given) + the right-hand side; returns (plan, out (ncomp, n_rows))."""
     k = RHS_KINDS[kind] if isinstance(kind, str) else int(kind)
@@ -351,6 +352,8 @@ def assemble_rhs(mesh_arrays, u, kind="load", row_begin=0, row_end=None, device=
         m = lfem_mesh_create(mesh_arrays.domain, mesh_arrays.order, mesh_arrays.quad, coords, conn)
         plan = lfem_assemble_symbolic(m, row_begin, row_end)
         plan._keep = (coords, conn)
+    if variant is not None:
+        lfem_plan_set_variant(plan, variant)
     uu = torch.as_tensor(u, dtype=torch.float64, device=device).reshape(nc, -1).contiguous()
     out = torch.empty((nc, plan.n_rows), dtype=torch.float64, device=device)
     lfem_assemble_rhs(plan, k, None, uu, out)

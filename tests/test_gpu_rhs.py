@@ -64,23 +64,49 @@ BULK = [
 ]
 
 
+VARIANTS = [lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED]
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=["v0", "fused"])
 @pytest.mark.parametrize("name,mk", SURF + BULK, ids=[s[0] for s in SURF + BULK])
-def test_load_parity(name, mk):
+def test_load_parity(name, mk, variant):
     m = mk()
     u = fields(m, "load")
-    plan, out = lfem.assemble_rhs(m, u, "load")
+    plan, out = lfem.assemble_rhs(m, u, "load", variant=variant)
     o, oabs = oracle.assemble_rhs_rows(m, u, "load", with_abs=True)
     check(out.cpu().numpy(), o, oabs)
-    assert lfem.lfem_rhs_launches(plan, lfem.LFEM_RHS_LOAD) == 2
+    assert lfem.lfem_rhs_launches(plan, lfem.LFEM_RHS_LOAD) == (2 if variant == lfem.LFEM_NUMERIC_V0 else 1)
+    if variant == lfem.LFEM_NUMERIC_V0:
+        _, out2 = lfem.assemble_rhs(m, u, "load", plan=plan, variant=lfem.LFEM_NUMERIC_TILED)
+        assert torch.equal(out, out2)
 
 
+@pytest.mark.parametrize("variant", VARIANTS, ids=["v0", "fused"])
 @pytest.mark.parametrize("name,mk", SURF, ids=[s[0] for s in SURF])
-def test_kll_parity(name, mk):
+def test_kll_parity(name, mk, variant):
     m = mk()
     u = fields(m, "kll")
-    _, out = lfem.assemble_rhs(m, u, "kll")
+    _, out = lfem.assemble_rhs(m, u, "kll", variant=variant)
     o, oabs = oracle.assemble_rhs_rows(m, u, "kll", with_abs=True)
     check(out.cpu().numpy(), o, oabs)
+
+
+@pytest.mark.parametrize("kind", ["load", "kll"])
+def test_rhs_variants_bitwise(kind):
+    """The fused and the two-kernel variants sum the same element values in the same order."""
+    m = li.make_config("C5", level_override=6)
+    u = fields(m, kind)
+    _, a = lfem.assemble_rhs(m, u, kind, variant=lfem.LFEM_NUMERIC_V0)
+    plan, b = lfem.assemble_rhs(m, u, kind, variant=lfem.LFEM_NUMERIC_TILED)
+    assert lfem.lfem_rhs_launches(plan, lfem.RHS_KINDS[kind]) == 1
+    assert torch.equal(a, b)
+    # the matrices on the same plan after the rhs built its tile plan, and the rhs again after them
+    vals = [torch.empty(plan.nnz, dtype=torch.float64, device="cuda"), None, None]
+    lfem.lfem_assemble_numeric(plan, lfem.LFEM_MASS, None, vals)
+    _, c = lfem.assemble_rhs(m, u, kind, plan=plan)
+    assert torch.equal(a, c)
+    _, d = lfem.assemble_rhs(m, u, kind, plan=plan, variant=lfem.LFEM_NUMERIC_AUTO)  # AUTO = the two kernels
+    assert torch.equal(a, d) and lfem.lfem_rhs_launches(plan, lfem.RHS_KINDS[kind]) == 2
 
 
 def test_kll_identity_field_gives_2Mx():
@@ -110,8 +136,9 @@ def test_rhs_row_blocks_bitwise(kind):
     full = full.cpu().numpy()
     cuts = [0, 1, m.n_nodes // 3, m.n_nodes // 3 + 7, m.n_nodes - 5, m.n_nodes]
     for a, b in zip(cuts[:-1], cuts[1:]):
-        _, part = lfem.assemble_rhs(m, u, kind, row_begin=a, row_end=b)
-        assert np.array_equal(part.cpu().numpy(), full[:, a:b]), (a, b)
+        for variant in VARIANTS:
+            _, part = lfem.assemble_rhs(m, u, kind, row_begin=a, row_end=b, variant=variant)
+            assert np.array_equal(part.cpu().numpy(), full[:, a:b]), (a, b, variant)
 
 
 @pytest.mark.parametrize("kind", ["load", "kll"])

@@ -248,3 +248,16 @@ def test_rhs_errors():
     with pytest.raises(oracle.OracleError) as ei:
         oracle.assemble_rhs_rows(deg, np.ones((1, m.n_nodes)), "load")
     assert ei.value.code == 4
+
+
+def test_abs_scale_is_the_value_for_nonnegative_terms():
+    """The tolerance scale (absolute-value evaluation, reading G33) equals the value when every
+    term is nonnegative (P1, f > 0; KLL with nu = x on a flat P1 mesh, H > 0) and bounds it otherwise."""
+    m = plane_mesh(3, 1)
+    f = 1.0 + 0.5 * (li.random_field(m, 3) + 1.0)
+    b, babs = oracle.assemble_rhs_rows(m, f[None, :], "load", with_abs=True)
+    assert np.allclose(b, babs, rtol=1e-14, atol=0)
+    m2 = li.sphere_mesh(1, 2)
+    f2 = li.random_field(m2, 4)
+    b2, babs2 = oracle.assemble_rhs_rows(m2, f2[None, :], "load", with_abs=True)
+    assert np.all(babs2 >= np.abs(b2)) and np.any(babs2 > 2 * np.abs(b2))
