@@ -607,3 +607,12 @@ def perturb(m: Mesh, seed: int, eps: float) -> Mesh:
     c = m.coords + eps * (2.0 * u - 1.0)
     return _finish(Mesh(m.domain, m.order, c, m.conn.copy(), m.quad,
                         None if m.coeff is None else m.coeff.copy()))
+
+
+def dziuk_surface(level: int, order: int = 2, sfc: bool = True) -> Mesh:
+    """PAPER.md P:842 (Dziuk's MCF example): the sphere's nodes mapped by
+    x -> (1 + 0.5 sin(2 pi (x + y)) cos(0.25 z pi)) x."""
+    m = sphere_mesh(level, order, sfc=sfc)
+    x = m.coords
+    s = 1.0 + 0.5 * np.sin(2.0 * math.pi * (x[:, 0] + x[:, 1])) * np.cos(0.25 * x[:, 2] * math.pi)
+    return _finish(Mesh(m.domain, m.order, s[:, None] * x, m.conn, m.quad))
