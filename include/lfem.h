@@ -200,6 +200,29 @@ int lfem_rhs_ncomp(int kind);
 /* Kernel launches the plan's last lfem_assemble_rhs call enqueued (1 fused, 2 two-kernel). */
 int lfem_rhs_launches(lfem_plan p, int kind);
 
+/* Jacobi-preconditioned conjugate gradients for K x = b with three right-hand
+ * sides at once, K = the plan's CSR pattern with
+ * values vals_K (device, nnz fp64, BORROWED; symmetric positive definite with a
+ * positive diagonal).  b, x: device n_nodes x 3 AoS (the node array's layout);
+ * x holds the initial guess on entry and the solution on exit.  Stops when
+ * ||r_k|| <= tol ||b_k|| for every column k, else LFEM_ERR_STATE after max_it
+ * iterations.  Whole-mesh plans only (UNSUPPORTED for a row block: the
+ * multi-GPU solve would need an exchange per iteration).  Deterministic
+ * reductions; synchronises `stream` once per iteration (convergence check).
+ * iters (host, may be NULL): iterations used.  Plan-owned workspace. */
+lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, double* x, double tol,
+                          int max_it, int* iters, lfem_stream_t stream);
+
+/* One step of Dziuk's algorithm for mean curvature flow:
+ *     (M(x^{n-1}) + tau A(x^{n-1})) x^n = M(x^{n-1}) x^{n-1}
+ * on a whole-mesh surface plan: numeric assembly of M and A at x_prev (the
+ * plan's topology; x_prev replaces the mesh coordinates), K = M + tau A,
+ * b = M x_prev, then lfem_cg_solve from the initial guess x_prev.
+ * x_prev, x_next: device n_nodes x 3 (may alias).  tau > 0.  UNSUPPORTED on
+ * bulk meshes.  Degenerate elements are latched (lfem_plan_check). */
+lfem_status lfem_mcf_step(lfem_plan p, double tau, const double* x_prev, double* x_next, double tol,
+                          int max_it, int* iters, lfem_stream_t stream);
+
 /* CSR pattern of the plan: device pointers, PLAN-OWNED.
  * row_ptr: n_rows + 1 int64 (relative to the block); col_idx: nnz int32 (global). */
 lfem_status lfem_csr_get(lfem_plan p, const int64_t** row_ptr, const int32_t** col_idx);

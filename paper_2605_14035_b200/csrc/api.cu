@@ -90,6 +90,7 @@ void free_plan_memory(lfem_plan_s* p) {
     dev_free(p->rhs_codes, s);
     dev_free(p->rhs_stage, s);
     dev_free(p->rhs_tcodes, s);
+    mcf_free(p, s);
     free_tiles(p->tiles, s);
     delete p->prof;
     p->prof = nullptr;
@@ -401,6 +402,29 @@ lfem_status lfem_assemble_rhs(lfem_plan p, int kind, const double* coords, const
     if (!u && p->mesh->n_nodes > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "u is NULL");
     if (!out && p->n_rows > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "out is NULL");
     return rhs_dispatch(p, kind, coords ? coords : p->mesh->coords, u, out, S(stream));
+}
+
+lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, double* x, double tol, int max_it,
+                          int* iters, lfem_stream_t stream) {
+    g_err.clear();
+    g_err_elem = -1;
+    if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
+    if (p->n_rows > 0 && (!vals_K || !b || !x)) return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL argument");
+    if (!(tol > 0.0) || max_it < 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "tol must be > 0 and max_it >= 0");
+    return cg_solve(p, vals_K, b, x, tol, max_it, iters, S(stream));
+}
+
+lfem_status lfem_mcf_step(lfem_plan p, double tau, const double* x_prev, double* x_next, double tol, int max_it,
+                          int* iters, lfem_stream_t stream) {
+    g_err.clear();
+    g_err_elem = -1;
+    if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
+    if (p->mesh->domain != LFEM_SURFACE_TRI)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "Dziuk's MCF step is defined for surfaces");
+    if (p->n_rows > 0 && (!x_prev || !x_next)) return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL argument");
+    if (!(tau > 0.0) || !(tol > 0.0) || max_it < 0)
+        return lfem_fail(LFEM_ERR_INVALID_ARG, "tau and tol must be > 0, max_it >= 0");
+    return mcf_step(p, tau, x_prev, x_next, tol, max_it, iters, S(stream));
 }
 
 lfem_status lfem_plan_check(lfem_plan p, lfem_stream_t stream) {

@@ -53,6 +53,12 @@ struct TilePlan {
     uint16_t* heavy = nullptr;          // per heavy slot: [slot - s0, count, codes...] (fixed size per family)
     bool ready = false;
 };
+// Workspace of lfem_cg_solve / lfem_mcf_step (mcf.cu): AoS n x 3 vectors, M/A/K values
+struct McfWork {
+    double *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr, *b = nullptr, *dinv = nullptr;
+    double *M = nullptr, *A = nullptr, *K = nullptr, *part = nullptr, *sc = nullptr;
+    int* bad = nullptr;
+};
 struct Profiler;  // api.cu
 void prof_begin(lfem_plan_s* p, const char* name, cudaStream_t s);
 void prof_end(lfem_plan_s* p, cudaStream_t s);
@@ -83,6 +89,7 @@ struct lfem_plan_s {
     uint16_t* rhs_tcodes = nullptr; // fused variant: e_tile * nref + a, same indexing as rhs_codes
     int rhs_tiled = -1;             // -1 not tried, 0 unavailable, 1 tile-local codes built
     int rhs_last_tiled = -1;        // variant of the last lfem_assemble_rhs call (1 fused, 0 two-kernel)
+    McfWork mcf;                    // CG / MCF workspace (mcf.cu)
 };
 
 // ---------------------------------------------------------------------------
@@ -154,6 +161,12 @@ int numeric_launch_count(lfem_plan_s* p, unsigned kinds);
 lfem_status rhs_dispatch(lfem_plan_s* p, int kind, const double* coords, const double* u, double* out,
                          cudaStream_t s);
 int rhs_launch_count(lfem_plan_s* p);
+// mcf.cu
+lfem_status cg_solve(lfem_plan_s* p, const double* vals_K, const double* b, double* x, double tol, int max_it,
+                     int* iters, cudaStream_t s);
+lfem_status mcf_step(lfem_plan_s* p, double tau, const double* x_prev, double* x_next, double tol, int max_it,
+                     int* iters, cudaStream_t s);
+void mcf_free(lfem_plan_s* p, cudaStream_t s);
 lfem_status spmv_launch(lfem_plan_s* p, const double* vals, const double* x, double* y, cudaStream_t s);
 lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const double* b, double* out,
                          cudaStream_t s);

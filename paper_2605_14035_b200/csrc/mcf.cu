@@ -1,0 +1,288 @@
+// Dziuk's algorithm for mean curvature flow on B200.
+//
+// the linearly implicit Euler / ESFEM discretisation of
+// d/dt X = Laplace_{Gamma[X]} Id reads
+//     (M(x^{n-1}) + tau A(x^{n-1})) x^n = M(x^{n-1}) x^{n-1},
+// one system per coordinate.  One step here = the numeric assembly of M and A
+// at x^{n-1} (the hot path, on the plan's fixed topology: symbolic once), K =
+// M + tau A (lfem_axpby's kernel), b = M x^{n-1}, and a Jacobi-preconditioned
+// conjugate gradient solve of the three systems at once.
+//
+// Vectors are n x 3 AoS (the node array's own layout), so K's values and
+// column indices are read once per iteration for all three coordinates
+// (k_spmm3).  Dot products are deterministic: fixed grid, per-block tree
+// reduction, then a one-block final pass in block order.  Convergence is
+// checked on the host after every iteration (one 24-B read).
+#include <climits>
+#include <cmath>
+#include <vector>
+
+#include "lfem_internal.cuh"
+
+namespace {
+
+constexpr int DOT_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int DOT_THREADS = 256;
+
+inline unsigned grid_rows(int64_t n, int per_block) {
+    int64_t g = (n + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > (1 << 20)) g = 1 << 20;
+    return (unsigned)g;
+}
+
+// Y[i] = sum_j K_ij X[col_j] (3 columns, AoS); warp per row, fixed-order reduction
+__global__ void k_spmm3(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                        const double* __restrict__ vals, const double* __restrict__ X, double* __restrict__ Y) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t r = w; r < n; r += nw) {
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+        for (int64_t j = row_ptr[r] + lane; j < row_ptr[r + 1]; j += 32) {
+            const double v = __ldg(&vals[j]);
+            const int64_t c = __ldg(&col[j]);
+            a0 = fma(v, __ldg(&X[3 * c]), a0);
+            a1 = fma(v, __ldg(&X[3 * c + 1]), a1);
+            a2 = fma(v, __ldg(&X[3 * c + 2]), a2);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            a0 += __shfl_down_sync(0xffffffffu, a0, o);
+            a1 += __shfl_down_sync(0xffffffffu, a1, o);
+            a2 += __shfl_down_sync(0xffffffffu, a2, o);
+        }
+        if (lane == 0) {
+            Y[3 * r] = a0;
+            Y[3 * r + 1] = a1;
+            Y[3 * r + 2] = a2;
+        }
+    }
+}
+
+// dinv[i] = 1 / K_ii (binary search of the diagonal among the row's sorted columns)
+__global__ void k_diag_inv(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                           const double* __restrict__ vals, double* __restrict__ dinv, int* __restrict__ bad) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = row_ptr[i], hi = row_ptr[i + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col[mid] < i) lo = mid + 1;
+            else hi = mid;
+        }
+        const bool found = lo < row_ptr[i + 1] && col[lo] == i && vals[lo] > 0.0;
+        dinv[i] = found ? 1.0 / vals[lo] : 1.0;
+        if (!found) atomicMin(bad, (int)i);
+    }
+}
+
+// block-level sum of 3 (or 6) per-thread values into part[blockIdx][k], fixed order
+template <int K>
+__device__ __forceinline__ void block_sums(double (&v)[K], double* __restrict__ part) {
+    __shared__ double sh[DOT_THREADS / 32][K];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_down_sync(0xffffffffu, v[k], o);
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[warp][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double s = 0.0;
+        for (int w = 0; w < DOT_THREADS / 32; ++w) s += sh[w][threadIdx.x];
+        part[blockIdx.x * K + threadIdx.x] = s;
+    }
+}
+
+// out[k] = sum of part[b][k] over blocks in order (one block of 32 * K threads would do; one warp suffices)
+template <int K>
+__global__ void k_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+    if (threadIdx.x < K) {
+        double s = 0.0;
+        for (int b = 0; b < nb; ++b) s += part[b * K + threadIdx.x];
+        out[threadIdx.x] = s;
+    }
+}
+
+// r = b - K x (q holds K x), z = dinv r, p = z; partials of r.z and r.r, per column
+__global__ void __launch_bounds__(DOT_THREADS) k_cg_init(int64_t n, const double* __restrict__ b,
+                                                         const double* __restrict__ q, const double* __restrict__ dinv,
+                                                         double* __restrict__ r, double* __restrict__ z,
+                                                         double* __restrict__ p, double* __restrict__ part) {
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = dinv[i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const double rr = b[3 * i + k] - q[3 * i + k];
+            const double zz = d * rr;
+            r[3 * i + k] = rr;
+            z[3 * i + k] = zz;
+            p[3 * i + k] = zz;
+            v[k] = fma(rr, zz, v[k]);
+            v[3 + k] = fma(rr, rr, v[3 + k]);
+        }
+    }
+    block_sums<6>(v, part);
+}
+
+// partials of p.q per column
+__global__ void __launch_bounds__(DOT_THREADS) k_dot_pq(int64_t n, const double* __restrict__ p,
+                                                        const double* __restrict__ q, double* __restrict__ part) {
+    double v[3] = {0, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] = fma(p[3 * i + k], q[3 * i + k], v[k]);
+    block_sums<3>(v, part);
+}
+
+// alpha_k = rz_k / pq_k (0 for a converged column); x += alpha p, r -= alpha q, z = dinv r;
+// partials of the new r.z and r.r.   s: [rz(3), rr(3), pq(3)]
+__global__ void __launch_bounds__(DOT_THREADS) k_cg_update(int64_t n, const double* __restrict__ s,
+                                                           const double* __restrict__ p, const double* __restrict__ q,
+                                                           const double* __restrict__ dinv, double* __restrict__ x,
+                                                           double* __restrict__ r, double* __restrict__ z,
+                                                           double* __restrict__ part) {
+    double al[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) al[k] = s[6 + k] != 0.0 ? s[k] / s[6 + k] : 0.0;
+    double v[6] = {0, 0, 0, 0, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = dinv[i];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            x[3 * i + k] = fma(al[k], p[3 * i + k], x[3 * i + k]);
+            const double rr = fma(-al[k], q[3 * i + k], r[3 * i + k]);
+            const double zz = d * rr;
+            r[3 * i + k] = rr;
+            z[3 * i + k] = zz;
+            v[k] = fma(rr, zz, v[k]);
+            v[3 + k] = fma(rr, rr, v[3 + k]);
+        }
+    }
+    block_sums<6>(v, part);
+}
+
+// p = z + beta p, beta_k = rz_new_k / rz_old_k; then rz_old = rz_new
+__global__ void k_cg_dir(int64_t n, const double* __restrict__ s_new, double* __restrict__ s_old,
+                         const double* __restrict__ z, double* __restrict__ p) {
+    double be[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) be[k] = s_old[k] != 0.0 ? s_new[k] / s_old[k] : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) p[3 * i + k] = fma(be[k], p[3 * i + k], z[3 * i + k]);
+}
+
+__global__ void k_copy_rz(const double* __restrict__ src, double* __restrict__ dst) {
+    if (threadIdx.x < 3) dst[threadIdx.x] = src[threadIdx.x];
+}
+
+}  // namespace
+
+// Workspace of the CG / MCF entry points (plan-owned, lfem_internal.cuh's McfWork).
+static lfem_status mcf_work(lfem_plan_s* p, cudaStream_t s) {
+    McfWork& W = p->mcf;
+    if (W.r) return LFEM_OK;
+    const int64_t n = p->n_rows, nnz = p->nnz;
+    for (double** v : {&W.r, &W.z, &W.pv, &W.q, &W.b}) LFEM_TRY(dev_alloc_t(v, (size_t)3 * n + 3, s));
+    LFEM_TRY(dev_alloc_t(&W.dinv, (size_t)n + 1, s));
+    for (double** v : {&W.M, &W.A, &W.K}) LFEM_TRY(dev_alloc_t(v, (size_t)nnz + 1, s));
+    LFEM_TRY(dev_alloc_t(&W.part, (size_t)DOT_BLOCKS * 6, s));
+    LFEM_TRY(dev_alloc_t(&W.sc, 16, s));
+    LFEM_TRY(dev_alloc_t(&W.bad, 1, s));
+    return LFEM_OK;
+}
+
+void mcf_free(lfem_plan_s* p, cudaStream_t s) {
+    McfWork& W = p->mcf;
+    for (void* v : {(void*)W.r, (void*)W.z, (void*)W.pv, (void*)W.q, (void*)W.b, (void*)W.dinv, (void*)W.M,
+                    (void*)W.A, (void*)W.K, (void*)W.part, (void*)W.sc, (void*)W.bad})
+        dev_free(v, s);
+    W = McfWork{};
+}
+
+static lfem_status whole_mesh(lfem_plan_s* p) {
+    if (p->row_begin != 0 || p->row_end != p->mesh->n_nodes)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "CG / MCF need a whole-mesh plan (row block given)");
+    return LFEM_OK;
+}
+
+// CG on K (plan pattern, values vals_K) for the three AoS columns of b; x: initial guess in, solution out.
+static lfem_status cg_run(lfem_plan_s* p, const double* vals_K, const double* b, double* x, double tol, int max_it,
+                          int* iters_out, cudaStream_t s) {
+    McfWork& W = p->mcf;
+    const int64_t n = p->n_rows;
+    if (iters_out) *iters_out = 0;
+    if (n == 0) return LFEM_OK;
+    const unsigned gsp = grid_rows(n * 32, 256);
+    LFEM_CUDA(cudaMemsetAsync(W.bad, 0x7f, sizeof(int), s));
+    k_diag_inv<<<grid_rows(n, 256), 256, 0, s>>>(n, p->row_ptr, p->col_idx, vals_K, W.dinv, W.bad);
+    LFEM_CUDA(cudaGetLastError());
+    // ||b_k||
+    double* S = W.sc;  // [0..2] rz, [3..5] rr, [6..8] pq, [9..11] rz_new, [12..14] rr_new (+ pad)
+    k_dot_pq<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, b, b, W.part);
+    k_final<3><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 6);
+    double bb[3];
+    int hbad = 0;
+    LFEM_CUDA(cudaMemcpyAsync(bb, S + 6, sizeof(bb), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaMemcpyAsync(&hbad, W.bad, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    if (hbad != 0x7f7f7f7f) return lfem_fail(LFEM_ERR_STATE, "K has a zero or negative diagonal entry", hbad);
+    // r = b - K x, z = D^-1 r, p = z
+    k_spmm3<<<gsp, 256, 0, s>>>(n, p->row_ptr, p->col_idx, vals_K, x, W.q);
+    k_cg_init<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, b, W.q, W.dinv, W.r, W.z, W.pv, W.part);
+    k_final<6><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S);
+    LFEM_CUDA(cudaGetLastError());
+    double rr[6];
+    for (int it = 0;; ++it) {
+        LFEM_CUDA(cudaMemcpyAsync(rr, S + (it == 0 ? 0 : 9), sizeof(rr), cudaMemcpyDeviceToHost, s));
+        LFEM_CUDA(cudaStreamSynchronize(s));
+        bool done = true;
+        for (int k = 0; k < 3; ++k) {
+            if (!std::isfinite(rr[3 + k])) return lfem_fail(LFEM_ERR_STATE, "CG diverged (non-finite residual)");
+            done &= std::sqrt(rr[3 + k]) <= tol * std::sqrt(bb[k]);
+        }
+        if (iters_out) *iters_out = it;
+        if (done) return LFEM_OK;
+        if (it >= max_it) return lfem_fail(LFEM_ERR_STATE, "CG did not converge within max_it iterations");
+        if (it > 0) {  // p = z + beta p with beta = rz_new / rz, rz <- rz_new
+            k_cg_dir<<<grid_rows(n, 256), 256, 0, s>>>(n, S + 9, S, W.z, W.pv);
+            k_copy_rz<<<1, 32, 0, s>>>(S + 9, S);
+        }
+        k_spmm3<<<gsp, 256, 0, s>>>(n, p->row_ptr, p->col_idx, vals_K, W.pv, W.q);
+        k_dot_pq<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, W.pv, W.q, W.part);
+        k_final<3><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 6);
+        k_cg_update<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, S, W.pv, W.q, W.dinv, x, W.r, W.z, W.part);
+        k_final<6><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 9);
+        LFEM_CUDA(cudaGetLastError());
+    }
+}
+
+lfem_status cg_solve(lfem_plan_s* p, const double* vals_K, const double* b, double* x, double tol, int max_it,
+                     int* iters, cudaStream_t s) {
+    LFEM_TRY(whole_mesh(p));
+    LFEM_TRY(mcf_work(p, s));
+    return cg_run(p, vals_K, b, x, tol, max_it, iters, s);
+}
+
+lfem_status mcf_step(lfem_plan_s* p, double tau, const double* x_prev, double* x_next, double tol, int max_it,
+                     int* iters, cudaStream_t s) {
+    LFEM_TRY(whole_mesh(p));
+    LFEM_TRY(mcf_work(p, s));
+    McfWork& W = p->mcf;
+    const int64_t n = p->n_rows;
+    // M, A at x^{n-1} (the assembly hot path on the fixed plan)
+    double* vals[3] = {W.M, W.A, nullptr};
+    LFEM_TRY(numeric_dispatch(p, LFEM_MASS | LFEM_STIFF, x_prev, nullptr, vals, s));
+    LFEM_TRY(axpby_launch(p->nnz, 1.0, W.M, tau, W.A, W.K, s));  // K = M + tau A
+    if (n > 0) {
+        k_spmm3<<<grid_rows(n * 32, 256), 256, 0, s>>>(n, p->row_ptr, p->col_idx, W.M, x_prev, W.b);  // b = M x^{n-1}
+        LFEM_CUDA(cudaGetLastError());
+        if (x_next != x_prev)
+            LFEM_CUDA(cudaMemcpyAsync(x_next, x_prev, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
+    }
+    return cg_run(p, W.K, W.b, x_next, tol, max_it, iters, s);  // warm start: x^{n-1}
+}

@@ -36,7 +36,7 @@ EXPORTED = ("lfem_mesh_create", "lfem_mesh_destroy", "lfem_assemble_symbolic", "
             "lfem_assemble_numeric_host", "lfem_csr_get", "lfem_spmv", "lfem_plan_check", "lfem_axpby",
             "lfem_numeric_launches", "lfem_error_element", "lfem_last_error", "lfem_version",
             "lfem_profile_enable", "lfem_profile_read", "lfem_set_allocator", "lfem_assemble_rhs",
-            "lfem_rhs_ncomp", "lfem_rhs_launches")
+            "lfem_rhs_ncomp", "lfem_rhs_launches", "lfem_cg_solve", "lfem_mcf_step")
 
 
 class LfemError(RuntimeError):
@@ -84,6 +84,8 @@ def _lib():
         L.lfem_assemble_rhs.argtypes = [vp, c_int, vp, vp, vp, vp]
         L.lfem_rhs_ncomp.argtypes = [c_int]
         L.lfem_rhs_launches.argtypes = [vp, c_int]
+        L.lfem_cg_solve.argtypes = [vp, vp, vp, vp, ctypes.c_double, c_int, ctypes.POINTER(c_int), vp]
+        L.lfem_mcf_step.argtypes = [vp, ctypes.c_double, vp, vp, ctypes.c_double, c_int, ctypes.POINTER(c_int), vp]
         _LIB = L
     return _LIB
 
@@ -248,6 +250,27 @@ def lfem_assemble_rhs(plan: Plan, kind: int, coords: Optional[torch.Tensor], u: 
     out (ncomp, n_rows) fp64 on the device (component-major); coords None = the mesh's."""
     st = _lib().lfem_assemble_rhs(plan.handle, kind, _dptr(coords), _dptr(u), _dptr(out), _stream(stream))
     _check(st, "lfem_assemble_rhs")
+
+
+def lfem_cg_solve(plan: Plan, vals_K: torch.Tensor, b: torch.Tensor, x: torch.Tensor, tol: float = 1e-12,
+                  max_it: int = 10000, stream=None) -> int:
+    """K x = b for the three AoS columns of b (n_nodes x 3); x: initial guess in, solution out.
+    Returns the iterations used."""
+    it = ctypes.c_int(0)
+    st = _lib().lfem_cg_solve(plan.handle, _dptr(vals_K), _dptr(b), _dptr(x), tol, max_it, ctypes.byref(it),
+                              _stream(stream))
+    _check(st, "lfem_cg_solve")
+    return it.value
+
+
+def lfem_mcf_step(plan: Plan, tau: float, x_prev: torch.Tensor, x_next: torch.Tensor, tol: float = 1e-12,
+                  max_it: int = 10000, stream=None) -> int:
+    """One step of Dziuk's MCF on the device; returns the CG iterations."""
+    it = ctypes.c_int(0)
+    st = _lib().lfem_mcf_step(plan.handle, tau, _dptr(x_prev), _dptr(x_next), tol, max_it, ctypes.byref(it),
+                              _stream(stream))
+    _check(st, "lfem_mcf_step")
+    return it.value
 
 
 def lfem_plan_check(plan: Plan, stream=None):
