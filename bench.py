@@ -405,6 +405,130 @@ def run_rhs(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- GPU leg: Dziuk MCF (N3)
+MCF_LEVEL = {"C2": 7, "C5": 10}
+
+
+def run_mcf(args):
+    """One step = lfem_mcf_step (assembly of M, A at x^{n-1} + K = M + tau A + PCG for the three
+    coordinates) on the paper's Dziuk surface at the config's icosphere level, P2, tau = 0.005
+    (P:842).  The CG needs the whole mesh: with N ranks every rank runs an independent replica."""
+    import torch
+    import torch.distributed as dist
+
+    import lfem_inputs as li
+    from paper_2605_14035_b200 import lfem
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("LFEM_BENCH_DEVICE") is not None:
+        local = int(os.environ["LFEM_BENCH_DEVICE"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        backend = os.environ.get("LFEM_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, device_id=dev) if backend == "nccl" else dist.init_process_group(backend)
+    level = MCF_LEVEL.get(args.config, 7)
+    tau, tol = 0.005, 1e-10
+    t0 = time.time()
+    m = li.dziuk_surface(level, 2)
+    gen_s = time.time() - t0
+    coords = torch.as_tensor(m.coords).to(dev)
+    conn = torch.as_tensor(m.conn).to(dev)
+    mesh = lfem.lfem_mesh_create(m.domain, m.order, m.quad, coords, conn)
+    plan = lfem.lfem_assemble_symbolic(mesh, 0, m.n_nodes)
+    x = coords.clone()
+    y = torch.empty_like(x)
+    stream = torch.cuda.current_stream()
+    iters = []
+    for _ in range(args.warmup):
+        iters.append(lfem.lfem_mcf_step(plan, tau, x, y, tol=tol))
+        x, y = y, x
+    lfem.lfem_plan_check(plan)
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    it_timed = []
+    for _ in range(args.steps):
+        it_timed.append(lfem.lfem_mcf_step(plan, tau, x, y, tol=tol))
+        x, y = y, x
+    e1.record(stream)
+    torch.cuda.synchronize()
+    elapsed_ms = e0.elapsed_time(e1)
+    lfem.lfem_plan_check(plan)
+    # per-kernel profile over a few more steps (assembly kernel(s) and the CG SpMM)
+    lfem.lfem_profile_enable(plan, True)
+    nprof = 3
+    it_prof = []
+    t0p = torch.cuda.Event(enable_timing=True)
+    t1p = torch.cuda.Event(enable_timing=True)
+    t0p.record(stream)
+    for _ in range(nprof):
+        it_prof.append(lfem.lfem_mcf_step(plan, tau, x, y, tol=tol))
+        x, y = y, x
+    t1p.record(stream)
+    prof = lfem.lfem_profile_read(plan)
+    lfem.lfem_profile_enable(plan, False)
+    torch.cuda.synchronize()
+    prof_step_ms = t0p.elapsed_time(t1p) / nprof
+    clk = clocks.stop()
+    tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    elapsed_ms = float(tmax)
+    ms_per_step = elapsed_ms / args.steps
+    value = world * m.n_elems * args.steps / (elapsed_ms * 1e-3)
+    hbm, peak_src = peaks()
+    asm = {k: v for k, v in prof.items() if k != "k_spmm3"}
+    asm_ms = sum(v[0] for v in asm.values()) / nprof
+    spmm_ms, spmm_n = prof.get("k_spmm3", (0.0, 0))
+    n, nnz = m.n_nodes, plan.nnz
+    spmm_bytes = (n + 1) * 8 + nnz * 12 + 2 * n * 24
+    asm_bytes = algorithmic_bytes("C2", m.n_elems, m.nref, n, nnz, ("M", "A"), False)
+    if spmm_ms / nprof > asm_ms:
+        dom, dom_bytes, dom_ms = "k_spmm3", spmm_bytes, spmm_ms / max(1, spmm_n)
+    else:
+        dom, dom_bytes, dom_ms = "+".join(asm), asm_bytes, asm_ms
+    achieved = dom_bytes / (dom_ms * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                "traffic": None, "kernel": dom, "algorithmic_bytes_per_launch": int(dom_bytes), "kernel_ms": dom_ms,
+                "peak_source": peak_src,
+                "note": "k_spmm3 bytes: row_ptr + col + vals + x and y (each node once); K (nnz*12 B) may sit in L2"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import mcf as omcf
+        ms_ = li.dziuk_surface(5, 2)
+        t0 = time.perf_counter()
+        omcf.mcf_step(ms_, ms_.coords, tau)
+        dt = time.perf_counter() - t0
+        cpu = {"value": ms_.n_elems / dt, "unit": "elements/s", "cores": os.cpu_count() or 1, "kind": "oracle",
+               "sample": f"one oracle MCF step (std::map assembly + SuperLU direct solve) on the level-5 Dziuk "
+                         f"surface ({ms_.n_elems} elements, {dt:.2f} s); elements/s = n_elems / t"}
+    if rank == 0:
+        line = {"metric": "elements/s (Dziuk MCF steps: fp64 assembly of M, A + PCG solve of 3 coordinates)",
+                "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak" if world > 1 else "strong",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (the paper's Dziuk surface, P:842)",
+                "config": {"workload": f"Dziuk MCF on the P:842 surface, icosphere level {level} P2 ({m.n_elems} "
+                                       f"elements, {n} nodes), tau {tau}, CG tol {tol}",
+                           "parallelism": "replicas" if world > 1 else "1 GPU"},
+                "cg_iterations_mean": float(np.mean(it_timed)),
+                "assembly_ms_per_step": asm_ms, "spmm_ms_per_step": spmm_ms / nprof, "profiled_step_ms": prof_step_ms,
+                "assembly_share": asm_ms / prof_step_ms, "generate_s": gen_s,
+                "gpu_launches": None, "roofline": roofline, "clocks": clk, "e2e": None, "cpu_baseline": cpu}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
 # ----------------------------------------------------------------------------- GPU leg
 def run_lfem(args):
     import torch
@@ -705,6 +829,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--mcf", action="store_true",
+                    help="time Dziuk MCF steps (SURVEY §8(f) N3) on the paper's surface at the config's level")
     ap.add_argument("--rhs", default=None, choices=["load", "kll"],
                     help="time the right-hand side (SURVEY §8(f) N1) instead of the matrices")
     args = ap.parse_args()
@@ -715,6 +841,8 @@ def main():
         return run_reference(args)
     if args.rhs:
         return run_rhs(args)
+    if args.mcf:
+        return run_mcf(args)
     return run_lfem(args)
 
 

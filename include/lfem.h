@@ -208,7 +208,8 @@ int lfem_rhs_launches(lfem_plan p, int kind);
  * ||r_k|| <= tol ||b_k|| for every column k, else LFEM_ERR_STATE after max_it
  * iterations.  Whole-mesh plans only (UNSUPPORTED for a row block: the
  * multi-GPU solve would need an exchange per iteration).  Deterministic
- * reductions; synchronises `stream` once per iteration (convergence check).
+ * reductions; synchronises `stream` every 8 iterations (convergence check,
+ * so the iteration count is a multiple of 8 unless max_it is reached).
  * iters (host, may be NULL): iterations used.  Plan-owned workspace. */
 lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, double* x, double tol,
                           int max_it, int* iters, lfem_stream_t stream);

@@ -12,7 +12,7 @@
 // column indices are read once per iteration for all three coordinates
 // (k_spmm3).  Dot products are deterministic: fixed grid, per-block tree
 // reduction, then a one-block final pass in block order.  Convergence is
-// checked on the host after every iteration (one 24-B read).
+// checked on the host every CG_CHECK iterations (one 48-B read + sync).
 #include <climits>
 #include <cmath>
 #include <vector>
@@ -22,6 +22,7 @@
 namespace {
 
 constexpr int DOT_BLOCKS = 296;  // 2 x 148 SMs
+constexpr int CG_CHECK = 8;      // iterations between host convergence checks
 constexpr int DOT_THREADS = 256;
 
 inline unsigned grid_rows(int64_t n, int per_block) {
@@ -31,28 +32,34 @@ inline unsigned grid_rows(int64_t n, int per_block) {
     return (unsigned)g;
 }
 
-// Y[i] = sum_j K_ij X[col_j] (3 columns, AoS); warp per row, fixed-order reduction
+// Y[i] = sum_j K_ij X[col_j] (3 columns, AoS); SUB lanes per row (surface rows hold 7-19
+// entries: a whole warp per row would leave most lanes idle), fixed-order reduction
+constexpr int SPMM_SUB = 4;
 __global__ void k_spmm3(int64_t n, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
                         const double* __restrict__ vals, const double* __restrict__ X, double* __restrict__ Y) {
-    const int lane = threadIdx.x & 31;
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t r = w; r < n; r += nw) {
+    const int sl = threadIdx.x & (SPMM_SUB - 1);
+    const int64_t g = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / SPMM_SUB;
+    const int64_t ng = ((int64_t)gridDim.x * blockDim.x) / SPMM_SUB;
+    for (int64_t r0 = g; r0 < ((n + ng - 1) / ng) * ng; r0 += ng) {  // same trip count for every lane of a warp
+        const int64_t r = r0;
         double a0 = 0.0, a1 = 0.0, a2 = 0.0;
-        for (int64_t j = row_ptr[r] + lane; j < row_ptr[r + 1]; j += 32) {
-            const double v = __ldg(&vals[j]);
-            const int64_t c = __ldg(&col[j]);
-            a0 = fma(v, __ldg(&X[3 * c]), a0);
-            a1 = fma(v, __ldg(&X[3 * c + 1]), a1);
-            a2 = fma(v, __ldg(&X[3 * c + 2]), a2);
+        if (r < n) {
+            const int64_t j1 = __ldg(&row_ptr[r + 1]);
+            for (int64_t j = __ldg(&row_ptr[r]) + sl; j < j1; j += SPMM_SUB) {
+                const double v = __ldg(&vals[j]);
+                const int64_t c = __ldg(&col[j]);
+                a0 = fma(v, __ldg(&X[3 * c]), a0);
+                a1 = fma(v, __ldg(&X[3 * c + 1]), a1);
+                a2 = fma(v, __ldg(&X[3 * c + 2]), a2);
+            }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            a0 += __shfl_down_sync(0xffffffffu, a0, o);
-            a1 += __shfl_down_sync(0xffffffffu, a1, o);
-            a2 += __shfl_down_sync(0xffffffffu, a2, o);
+        for (int o = SPMM_SUB / 2; o > 0; o >>= 1) {
+            a0 += __shfl_down_sync(0xffffffffu, a0, o, SPMM_SUB);
+            a1 += __shfl_down_sync(0xffffffffu, a1, o, SPMM_SUB);
+            a2 += __shfl_down_sync(0xffffffffu, a2, o, SPMM_SUB);
         }
-        if (lane == 0) {
+        if (sl == 0 && r < n) {
             Y[3 * r] = a0;
             Y[3 * r + 1] = a1;
             Y[3 * r + 2] = a2;
@@ -217,7 +224,7 @@ static lfem_status cg_run(lfem_plan_s* p, const double* vals_K, const double* b,
     const int64_t n = p->n_rows;
     if (iters_out) *iters_out = 0;
     if (n == 0) return LFEM_OK;
-    const unsigned gsp = grid_rows(n * 32, 256);
+    const unsigned gsp = grid_rows(n * SPMM_SUB, 256);
     LFEM_CUDA(cudaMemsetAsync(W.bad, 0x7f, sizeof(int), s));
     k_diag_inv<<<grid_rows(n, 256), 256, 0, s>>>(n, p->row_ptr, p->col_idx, vals_K, W.dinv, W.bad);
     LFEM_CUDA(cudaGetLastError());
@@ -238,21 +245,26 @@ static lfem_status cg_run(lfem_plan_s* p, const double* vals_K, const double* b,
     LFEM_CUDA(cudaGetLastError());
     double rr[6];
     for (int it = 0;; ++it) {
-        LFEM_CUDA(cudaMemcpyAsync(rr, S + (it == 0 ? 0 : 9), sizeof(rr), cudaMemcpyDeviceToHost, s));
-        LFEM_CUDA(cudaStreamSynchronize(s));
-        bool done = true;
-        for (int k = 0; k < 3; ++k) {
-            if (!std::isfinite(rr[3 + k])) return lfem_fail(LFEM_ERR_STATE, "CG diverged (non-finite residual)");
-            done &= std::sqrt(rr[3 + k]) <= tol * std::sqrt(bb[k]);
+        // convergence check (one small read + sync) every CHECK iterations and at max_it
+        if (it % CG_CHECK == 0 || it >= max_it) {
+            LFEM_CUDA(cudaMemcpyAsync(rr, S + (it == 0 ? 0 : 9), sizeof(rr), cudaMemcpyDeviceToHost, s));
+            LFEM_CUDA(cudaStreamSynchronize(s));
+            bool done = true;
+            for (int k = 0; k < 3; ++k) {
+                if (!std::isfinite(rr[3 + k])) return lfem_fail(LFEM_ERR_STATE, "CG diverged (non-finite residual)");
+                done &= std::sqrt(rr[3 + k]) <= tol * std::sqrt(bb[k]);
+            }
+            if (iters_out) *iters_out = it;
+            if (done) return LFEM_OK;
+            if (it >= max_it) return lfem_fail(LFEM_ERR_STATE, "CG did not converge within max_it iterations");
         }
-        if (iters_out) *iters_out = it;
-        if (done) return LFEM_OK;
-        if (it >= max_it) return lfem_fail(LFEM_ERR_STATE, "CG did not converge within max_it iterations");
         if (it > 0) {  // p = z + beta p with beta = rz_new / rz, rz <- rz_new
             k_cg_dir<<<grid_rows(n, 256), 256, 0, s>>>(n, S + 9, S, W.z, W.pv);
             k_copy_rz<<<1, 32, 0, s>>>(S + 9, S);
         }
+        prof_begin(p, "k_spmm3", s);
         k_spmm3<<<gsp, 256, 0, s>>>(n, p->row_ptr, p->col_idx, vals_K, W.pv, W.q);
+        prof_end(p, s);
         k_dot_pq<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, W.pv, W.q, W.part);
         k_final<3><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 6);
         k_cg_update<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, S, W.pv, W.q, W.dinv, x, W.r, W.z, W.part);
@@ -279,7 +291,7 @@ lfem_status mcf_step(lfem_plan_s* p, double tau, const double* x_prev, double* x
     LFEM_TRY(numeric_dispatch(p, LFEM_MASS | LFEM_STIFF, x_prev, nullptr, vals, s));
     LFEM_TRY(axpby_launch(p->nnz, 1.0, W.M, tau, W.A, W.K, s));  // K = M + tau A
     if (n > 0) {
-        k_spmm3<<<grid_rows(n * 32, 256), 256, 0, s>>>(n, p->row_ptr, p->col_idx, W.M, x_prev, W.b);  // b = M x^{n-1}
+        k_spmm3<<<grid_rows(n * SPMM_SUB, 256), 256, 0, s>>>(n, p->row_ptr, p->col_idx, W.M, x_prev, W.b);  // b = M x^{n-1}
         LFEM_CUDA(cudaGetLastError());
         if (x_next != x_prev)
             LFEM_CUDA(cudaMemcpyAsync(x_next, x_prev, sizeof(double) * 3 * n, cudaMemcpyDeviceToDevice, s));
