@@ -7,7 +7,8 @@ Checks: (1) the blocks cover every row once and are balanced; (2) the blocks'
 CSR, gathered, is bitwise the whole-mesh assembly (halo elements duplicated,
 only owned rows kept); (3) the verification step of bench.py -- NCCL/gloo
 all-gather of a sharded x, local SpMV on the owned rows, all-reduce of the
-checksums -- reproduces the whole-matrix SpMV; (4) max-over-ranks timing.
+checksums -- reproduces the whole-matrix SpMV; (4) max-over-ranks timing;
+(5) the same for the KLL right-hand side.
 """
 import os
 import socket
@@ -40,6 +41,10 @@ def _spmv(rp, ci, v, x):
     return y
 
 
+def _kll_u(m):
+    return np.vstack([m.coords.T, m.coeff[None, :]])
+
+
 def _worker(rank, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=WORLD)
@@ -66,9 +71,11 @@ def _worker(rank, port, out):
         bounds = partition_rows(mesh.conn, n_nodes, WORLD)
         r0, r1 = bounds[rank], bounds[rank + 1]
         blk = oracle.assemble_rows(mesh, ("M", "A", "Aa"), rows=np.arange(r0, r1, dtype=np.int64), nthreads=1)
+        # N1: the KLL right-hand side of the owned rows (same decomposition, no collective)
+        f_blk = oracle.assemble_rhs_rows(mesh, _kll_u(mesh), "kll", rows=np.arange(r0, r1, dtype=np.int64), nthreads=1)
         # (2) gather the blocks on rank 0
         objs = [None] * WORLD
-        dist.all_gather_object(objs, (r0, r1, blk.row_ptr, blk.col_idx, {k: v for k, v in blk.vals.items()}))
+        dist.all_gather_object(objs, (r0, r1, blk.row_ptr, blk.col_idx, {k: v for k, v in blk.vals.items()}, f_blk))
         # (3) verification SpMV: x sharded, all-gathered, local rows, checksum all-reduced
         x = mesh.coords[:, 0].copy()
         shard = (n_nodes + WORLD - 1) // WORLD
@@ -118,6 +125,9 @@ def test_row_blocks_gloo_world2():
     assert np.array_equal(glued, full.row_ptr)
     for k in ("M", "A", "Aa"):
         assert np.array_equal(np.concatenate([o[4][k] for o in objs]), full.vals[k])
+    # N1 right-hand side: the gathered row blocks == the whole-mesh vector, bit for bit
+    f_full = oracle.assemble_rhs_rows(m, _kll_u(m), "kll", nthreads=1)
+    assert np.array_equal(np.concatenate([o[5] for o in objs], axis=1), f_full)
     # (3) distributed SpMV checksum == whole-matrix values
     x = m.coords[:, 0]
     yf = _spmv(full.row_ptr, full.col_idx, full.vals["A"], x)
