@@ -529,6 +529,98 @@ def run_mcf(args):
     return 0
 
 
+# ----------------------------------------------------------------------------- GPU leg: surface Poisson (N4)
+def run_poisson(args):
+    """One step = the P:725-728 pipeline on the unit sphere (P2, icosphere level of the config):
+    numeric assembly of M and A, the load vectors b = M f_I of f = 6 u for u = x1x2, x2x3, x3x1
+    (lfem_assemble_rhs), and the mean-free solve of the three systems (lfem_solve_meanfree)."""
+    import torch
+
+    import lfem_inputs as li
+    from paper_2605_14035_b200 import lfem
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    level = MCF_LEVEL.get(args.config, 7)
+    m = li.sphere_mesh(level, 2)
+    x = m.coords
+    u = np.stack([x[:, 0] * x[:, 1], x[:, 1] * x[:, 2], x[:, 2] * x[:, 0]], axis=1)
+    coords = torch.as_tensor(m.coords).to(dev)
+    conn = torch.as_tensor(m.conn).to(dev)
+    mesh = lfem.lfem_mesh_create(m.domain, m.order, m.quad, coords, conn)
+    plan = lfem.lfem_assemble_symbolic(mesh, 0, m.n_nodes)
+    vals = [torch.empty(plan.nnz, dtype=torch.float64, device=dev) for _ in range(2)] + [None]
+    f = torch.as_tensor(np.ascontiguousarray((6.0 * u).T)).to(dev)
+    bc = torch.empty((3, m.n_nodes), dtype=torch.float64, device=dev)
+    b = torch.empty((m.n_nodes, 3), dtype=torch.float64, device=dev)
+    uh = torch.empty_like(b)
+    stream = torch.cuda.current_stream()
+    its = []
+
+    def step():
+        lfem.lfem_assemble_numeric(plan, lfem.LFEM_MASS | lfem.LFEM_STIFF, None, vals)
+        for k in range(3):
+            lfem.lfem_assemble_rhs(plan, lfem.LFEM_RHS_LOAD, None, f[k:k + 1], bc[k:k + 1])
+        b.copy_(bc.t())  # component-major -> AoS (the solver's layout)
+        its.append(lfem.lfem_solve_meanfree(plan, vals[1], b, uh, tol=1e-10))
+    for _ in range(args.warmup):
+        step()
+    lfem.lfem_plan_check(plan)
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    its.clear()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    lfem.lfem_profile_enable(plan, True)
+    t0p, t1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0p.record(stream)
+    step()
+    t1p.record(stream)
+    prof = lfem.lfem_profile_read(plan)
+    lfem.lfem_profile_enable(plan, False)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    prof_ms = t0p.elapsed_time(t1p)
+    asm_ms = sum(v[0] for k, v in prof.items() if k != "k_spmm3")
+    spmm_ms, spmm_n = prof.get("k_spmm3", (0.0, 1))
+    n, nnz = m.n_nodes, plan.nnz
+    spmm_bytes = (n + 1) * 8 + nnz * 12 + 2 * n * 24
+    hbm, peak_src = peaks()
+    achieved = spmm_bytes / (spmm_ms / max(1, spmm_n) * 1e-3) / 1e9
+    # accuracy of the run: ||u_h - u_I||_M per column (P:145-150)
+    e = uh - (torch.as_tensor(u).to(dev) - torch.as_tensor(u.mean(axis=0)).to(dev))
+    Me = torch.empty_like(e)
+    err = []
+    for k in range(3):
+        ek = e[:, k].contiguous()
+        y = torch.empty(n, dtype=torch.float64, device=dev)
+        lfem.lfem_spmv(plan, vals[0], ek, y)
+        err.append(float(torch.dot(ek, y)) ** 0.5)
+    del Me
+    line = {"metric": "elements/s (surface Poisson pipeline: fp64 M, A, 3 load vectors, mean-free PCG solve)",
+            "value": m.n_elems / (ms * 1e-3), "unit": "elements/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (unit sphere, u = x1x2 etc., f = 6u; P:727)",
+            "config": {"workload": f"P2 unit icosphere level {level} ({m.n_elems} elements, {n} nodes), 3 right-hand "
+                                   f"sides, PCG tol 1e-10", "parallelism": "1 GPU"},
+            "pcg_iterations_mean": float(np.mean(its)), "assembly_ms": asm_ms, "spmm_ms": spmm_ms,
+            "profiled_step_ms": prof_ms, "error_M_norm": err,
+            "gpu_launches": None,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                         "traffic": None, "kernel": "k_spmm3", "algorithmic_bytes_per_launch": int(spmm_bytes),
+                         "kernel_ms": spmm_ms / max(1, spmm_n), "peak_source": peak_src},
+            "clocks": clk, "e2e": None, "cpu_baseline": None}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 # ----------------------------------------------------------------------------- GPU leg
 def run_lfem(args):
     import torch
@@ -829,6 +921,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--verify", action="store_true")
+    ap.add_argument("--poisson", action="store_true",
+                    help="time the surface Poisson pipeline (SURVEY §8(f) N4) at the config's icosphere level")
     ap.add_argument("--mcf", action="store_true",
                     help="time Dziuk MCF steps (SURVEY §8(f) N3) on the paper's surface at the config's level")
     ap.add_argument("--rhs", default=None, choices=["load", "kll"],
@@ -843,6 +937,8 @@ def main():
         return run_rhs(args)
     if args.mcf:
         return run_mcf(args)
+    if args.poisson:
+        return run_poisson(args)
     return run_lfem(args)
 
 

@@ -214,6 +214,17 @@ int lfem_rhs_launches(lfem_plan p, int kind);
 lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, double* x, double tol,
                           int max_it, int* iters, lfem_stream_t stream);
 
+/* Mean-free surface Poisson solve:
+ * the least-squares solution of the bordered system [A; e^T] u = [b; 0]
+ * (e = ones), i.e. A u = b - mean(b) e with sum_j u_j = 0, for three AoS
+ * columns at once.  vals_A: the plan's stiffness values (device, BORROWED;
+ * symmetric positive semidefinite with kernel span{e}).  b, u: device
+ * n_nodes x 3 AoS; u is overwritten.  Jacobi-PCG from u = 0 to
+ * ||r_k|| <= tol ||b_k - mean(b_k)||, then the nodal mean is removed.
+ * Whole-mesh plans only; iters as for lfem_cg_solve. */
+lfem_status lfem_solve_meanfree(lfem_plan p, const double* vals_A, const double* b, double* u, double tol,
+                                int max_it, int* iters, lfem_stream_t stream);
+
 /* One step of Dziuk's algorithm for mean curvature flow:
  *     (M(x^{n-1}) + tau A(x^{n-1})) x^n = M(x^{n-1}) x^{n-1}
  * on a whole-mesh surface plan: numeric assembly of M and A at x_prev (the

@@ -414,6 +414,16 @@ lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, do
     return cg_solve(p, vals_K, b, x, tol, max_it, iters, S(stream));
 }
 
+lfem_status lfem_solve_meanfree(lfem_plan p, const double* vals_A, const double* b, double* u, double tol,
+                                int max_it, int* iters, lfem_stream_t stream) {
+    g_err.clear();
+    g_err_elem = -1;
+    if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
+    if (p->n_rows > 0 && (!vals_A || !b || !u)) return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL argument");
+    if (!(tol > 0.0) || max_it < 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "tol must be > 0 and max_it >= 0");
+    return solve_meanfree(p, vals_A, b, u, tol, max_it, iters, S(stream));
+}
+
 lfem_status lfem_mcf_step(lfem_plan p, double tau, const double* x_prev, double* x_next, double tol, int max_it,
                           int* iters, lfem_stream_t stream) {
     g_err.clear();

@@ -167,6 +167,8 @@ lfem_status cg_solve(lfem_plan_s* p, const double* vals_K, const double* b, doub
 lfem_status mcf_step(lfem_plan_s* p, double tau, const double* x_prev, double* x_next, double tol, int max_it,
                      int* iters, cudaStream_t s);
 void mcf_free(lfem_plan_s* p, cudaStream_t s);
+lfem_status solve_meanfree(lfem_plan_s* p, const double* vals_A, const double* b, double* u, double tol, int max_it,
+                           int* iters, cudaStream_t s);
 lfem_status spmv_launch(lfem_plan_s* p, const double* vals, const double* x, double* y, cudaStream_t s);
 lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const double* b, double* out,
                          cudaStream_t s);

@@ -183,6 +183,27 @@ __global__ void k_cg_dir(int64_t n, const double* __restrict__ s_new, double* __
         for (int k = 0; k < 3; ++k) p[3 * i + k] = fma(be[k], p[3 * i + k], z[3 * i + k]);
 }
 
+// partials of the column sums of an AoS n x 3 array
+__global__ void __launch_bounds__(DOT_THREADS) k_colsum3(int64_t n, const double* __restrict__ a,
+                                                         double* __restrict__ part) {
+    double v[3] = {0, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) v[k] += a[3 * i + k];
+    block_sums<3>(v, part);
+}
+
+// out[i][k] = a[i][k] - sum_k / n  (sum: device, 3 column sums); out may alias a
+__global__ void k_sub_mean3(int64_t n, const double* __restrict__ sum, const double* a, double* out) {
+    const double inv = 1.0 / (double)n;
+    const double m0 = sum[0] * inv, m1 = sum[1] * inv, m2 = sum[2] * inv;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        out[3 * i] = a[3 * i] - m0;
+        out[3 * i + 1] = a[3 * i + 1] - m1;
+        out[3 * i + 2] = a[3 * i + 2] - m2;
+    }
+}
+
 __global__ void k_copy_rz(const double* __restrict__ src, double* __restrict__ dst) {
     if (threadIdx.x < 3) dst[threadIdx.x] = src[threadIdx.x];
 }
@@ -198,7 +219,7 @@ static lfem_status mcf_work(lfem_plan_s* p, cudaStream_t s) {
     LFEM_TRY(dev_alloc_t(&W.dinv, (size_t)n + 1, s));
     for (double** v : {&W.M, &W.A, &W.K}) LFEM_TRY(dev_alloc_t(v, (size_t)nnz + 1, s));
     LFEM_TRY(dev_alloc_t(&W.part, (size_t)DOT_BLOCKS * 6, s));
-    LFEM_TRY(dev_alloc_t(&W.sc, 16, s));
+    LFEM_TRY(dev_alloc_t(&W.sc, 24, s));  // CG scalars [0, 15), column sums [16, 19)
     LFEM_TRY(dev_alloc_t(&W.bad, 1, s));
     return LFEM_OK;
 }
@@ -278,6 +299,32 @@ lfem_status cg_solve(lfem_plan_s* p, const double* vals_K, const double* b, doub
     LFEM_TRY(whole_mesh(p));
     LFEM_TRY(mcf_work(p, s));
     return cg_run(p, vals_K, b, x, tol, max_it, iters, s);
+}
+
+// Mean-free surface Poisson: the least-squares solution of the bordered
+// system [A; e^T] u = [b; 0] is A u = P b, e^T u = 0 with P the Euclidean projection onto e-perp
+// (= range A): b~ = b - mean(b), PCG from u = 0 (iterates stay in range A for this consistent
+// singular system), then u -= mean(u) to remove rounding drift along the kernel e.
+lfem_status solve_meanfree(lfem_plan_s* p, const double* vals_A, const double* b, double* u, double tol, int max_it,
+                           int* iters, cudaStream_t s) {
+    LFEM_TRY(whole_mesh(p));
+    LFEM_TRY(mcf_work(p, s));
+    McfWork& W = p->mcf;
+    const int64_t n = p->n_rows;
+    if (iters) *iters = 0;
+    if (n == 0) return LFEM_OK;
+    double* S = W.sc;
+    k_colsum3<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, b, W.part);
+    k_final<3><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 16);
+    k_sub_mean3<<<grid_rows(n, 256), 256, 0, s>>>(n, S + 16, b, W.b);
+    LFEM_CUDA(cudaMemsetAsync(u, 0, sizeof(double) * 3 * n, s));
+    LFEM_CUDA(cudaGetLastError());
+    LFEM_TRY(cg_run(p, vals_A, W.b, u, tol, max_it, iters, s));
+    k_colsum3<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, u, W.part);
+    k_final<3><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 16);
+    k_sub_mean3<<<grid_rows(n, 256), 256, 0, s>>>(n, S + 16, u, u);
+    LFEM_CUDA(cudaGetLastError());
+    return LFEM_OK;
 }
 
 lfem_status mcf_step(lfem_plan_s* p, double tau, const double* x_prev, double* x_next, double tol, int max_it,

@@ -36,7 +36,8 @@ EXPORTED = ("lfem_mesh_create", "lfem_mesh_destroy", "lfem_assemble_symbolic", "
             "lfem_assemble_numeric_host", "lfem_csr_get", "lfem_spmv", "lfem_plan_check", "lfem_axpby",
             "lfem_numeric_launches", "lfem_error_element", "lfem_last_error", "lfem_version",
             "lfem_profile_enable", "lfem_profile_read", "lfem_set_allocator", "lfem_assemble_rhs",
-            "lfem_rhs_ncomp", "lfem_rhs_launches", "lfem_cg_solve", "lfem_mcf_step")
+            "lfem_rhs_ncomp", "lfem_rhs_launches", "lfem_cg_solve", "lfem_mcf_step",
+            "lfem_solve_meanfree")
 
 
 class LfemError(RuntimeError):
@@ -85,6 +86,7 @@ def _lib():
         L.lfem_rhs_ncomp.argtypes = [c_int]
         L.lfem_rhs_launches.argtypes = [vp, c_int]
         L.lfem_cg_solve.argtypes = [vp, vp, vp, vp, ctypes.c_double, c_int, ctypes.POINTER(c_int), vp]
+        L.lfem_solve_meanfree.argtypes = [vp, vp, vp, vp, ctypes.c_double, c_int, ctypes.POINTER(c_int), vp]
         L.lfem_mcf_step.argtypes = [vp, ctypes.c_double, vp, vp, ctypes.c_double, c_int, ctypes.POINTER(c_int), vp]
         _LIB = L
     return _LIB
@@ -260,6 +262,16 @@ def lfem_cg_solve(plan: Plan, vals_K: torch.Tensor, b: torch.Tensor, x: torch.Te
     st = _lib().lfem_cg_solve(plan.handle, _dptr(vals_K), _dptr(b), _dptr(x), tol, max_it, ctypes.byref(it),
                               _stream(stream))
     _check(st, "lfem_cg_solve")
+    return it.value
+
+
+def lfem_solve_meanfree(plan: Plan, vals_A: torch.Tensor, b: torch.Tensor, u: torch.Tensor, tol: float = 1e-12,
+                        max_it: int = 20000, stream=None) -> int:
+    """Mean-free Poisson for the three AoS columns of b; u (n_nodes x 3) is overwritten."""
+    it = ctypes.c_int(0)
+    st = _lib().lfem_solve_meanfree(plan.handle, _dptr(vals_A), _dptr(b), _dptr(u), tol, max_it, ctypes.byref(it),
+                                    _stream(stream))
+    _check(st, "lfem_solve_meanfree")
     return it.value
 
 
