@@ -530,7 +530,7 @@ def displace_cube(x: np.ndarray, rng: SplitMix64) -> np.ndarray:
 # ---------------------------------------------------------------------------
 # BASELINE.json configs
 # ---------------------------------------------------------------------------
-CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")
+CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")  # BASELINE.json; "C4P1" = N2's P1 tets at scale
 
 
 def make_config(name: str, seed: int = 0, level_override: Optional[int] = None) -> Mesh:
@@ -574,6 +574,14 @@ def make_config(name: str, seed: int = 0, level_override: Optional[int] = None) 
         x = displace_cube(x, rng)
         x, t = sfc_reorder(x, t, 4)
         m = Mesh(BULK_TET, 2, x, t, QUAD_TET11_DEG4)
+        m.extra["kinds"] = ("M", "A")
+    elif name == "C4P1":
+        # SURVEY §8(f) N2 "P1 tets at scale": the C4 recipe with P1 tetrahedra (TET4_DEG2)
+        n = 96 if level_override is None else level_override
+        x, t = kuhn_cube(n, 1)
+        x = displace_cube(x, rng)
+        x, t = sfc_reorder(x, t, 4)
+        m = Mesh(BULK_TET, 1, x, t, QUAD_TET4_DEG2)
         m.extra["kinds"] = ("M", "A")
     elif name == "C5":
         L = 10 if level_override is None else level_override

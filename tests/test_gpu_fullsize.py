@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
 
 from paper_2605_14035_b200 import lfem  # noqa: E402
 
-KINDS = {"C2": ("M", "A"), "C3": ("M", "Aa"), "C4": ("M", "A"), "C5": ("M", "A", "Aa")}
+KINDS = {"C2": ("M", "A"), "C3": ("M", "Aa"), "C4": ("M", "A"), "C5": ("M", "A", "Aa"), "C4P1": ("M", "A")}
 
 
 def _run(name, coeff=None):
@@ -105,6 +105,16 @@ def test_C4_full():
     _check_sampled(m, kinds, rp, ci, vals, None)
     vol = _properties(m, kinds, plan, vals, None, 3)
     assert abs(vol - 1.0) < 1e-11  # reading G16: |Omega_h| = 1
+
+
+def test_C4P1_full():
+    """P1 tetrahedra at scale (C4's cube, 5.3M tets); nnz = 15n^3 + 21n^2 + 9n + 1."""
+    m, kinds, plan, rp, ci, vals = _run("C4P1")
+    n = 96
+    assert plan.nnz == 15 * n ** 3 + 21 * n ** 2 + 9 * n + 1
+    _check_sampled(m, kinds, rp, ci, vals, None)
+    vol = _properties(m, kinds, plan, vals, None, 3)
+    assert abs(vol - 1.0) < 1e-11
 
 
 def test_C5_full():

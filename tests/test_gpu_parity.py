@@ -42,6 +42,7 @@ SMALL = [
     ("C1", lambda: li.make_config("C1")),
     ("C3_L4", lambda: li.make_config("C3", level_override=4)),
     ("C4_n5", lambda: li.make_config("C4", level_override=5)),
+    ("C4P1_n6", lambda: li.make_config("C4P1", level_override=6)),
     ("C5_L4", lambda: li.make_config("C5", level_override=4)),
 ]
 

@@ -122,3 +122,12 @@ def test_configs_deterministic():
     b = li.make_config("C3", level_override=3)
     assert np.array_equal(a.coords, b.coords) and np.array_equal(a.conn, b.conn)
     assert np.array_equal(a.coeff, b.coeff)
+
+
+def test_c4p1_recipe():
+    """N2 "P1 tets at scale": C4's displaced Kuhn cube with P1 tetrahedra and the 4-point rule."""
+    m = li.make_config("C4P1", level_override=3)
+    assert m.domain == li.BULK_TET and m.order == 1 and m.quad == li.QUAD_TET4_DEG2
+    assert m.n_elems == 6 * 27 and m.n_nodes == 64 and m.extra["kinds"] == ("M", "A")
+    m2 = li.make_config("C4P1", level_override=3)
+    assert np.array_equal(m.coords, m2.coords) and np.array_equal(m.conn, m2.conn)
