@@ -286,7 +286,7 @@ def run_rhs(args):
     mesh = lfem.lfem_mesh_create(m.domain, m.order, m.quad, coords, conn)
     plan = lfem.lfem_assemble_symbolic(mesh, r0, r1)
     lfem.lfem_plan_set_variant(plan, {"auto": lfem.LFEM_NUMERIC_AUTO, "v0": lfem.LFEM_NUMERIC_V0,
-                                      "tiled": lfem.LFEM_NUMERIC_TILED}[args.variant])
+                                      "tiled": lfem.LFEM_NUMERIC_TILED, "rows": lfem.LFEM_NUMERIC_V0}[args.variant])
     out = torch.empty((nc, plan.n_rows), dtype=torch.float64, device=dev)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
@@ -697,7 +697,8 @@ def run_lfem(args):
     plan = lfem.lfem_assemble_symbolic(mesh, r0, r1)
     torch.cuda.synchronize()
     symbolic_ms = 1e3 * (time.perf_counter() - t0)
-    variant = {"auto": lfem.LFEM_NUMERIC_AUTO, "v0": lfem.LFEM_NUMERIC_V0, "tiled": lfem.LFEM_NUMERIC_TILED}[args.variant]
+    variant = {"auto": lfem.LFEM_NUMERIC_AUTO, "v0": lfem.LFEM_NUMERIC_V0, "tiled": lfem.LFEM_NUMERIC_TILED,
+               "rows": lfem.LFEM_NUMERIC_ROWS}[args.variant]
     lfem.lfem_plan_set_variant(plan, variant)
     vals = [None, None, None]
     for k in kinds:
@@ -917,7 +918,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "C4P1"])
     ap.add_argument("--impl", default="lfem", choices=["lfem", "reference"])
-    ap.add_argument("--variant", default="auto", choices=["auto", "v0", "tiled"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "v0", "tiled", "rows"])
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

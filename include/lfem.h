@@ -95,12 +95,16 @@ typedef enum {
 enum { LFEM_MASS = 1u, LFEM_STIFF = 2u, LFEM_STIFF_COEF = 4u };
 
 /* Numeric variants (lfem_plan_set_variant); all produce identical bits.
- * AUTO picks TILED for triangles and V0 for tetrahedra (measured). */
+ * AUTO picks TILED for triangles and V0 for tetrahedra (measured, DESIGN.md
+ * §6.5); ROWS is opt-in (measured slower: 2.4 vs 0.72 ms on C4P1). */
 typedef enum {
     LFEM_NUMERIC_AUTO = 0,   /* the fastest measured variant for the family */
     LFEM_NUMERIC_V0 = 1,     /* element kernel -> element-major local matrices in HBM -> per-slot gather */
-    LFEM_NUMERIC_TILED = 2   /* fused row-tile kernel: TMA-fed, warp-specialised, shared-memory stage,
+    LFEM_NUMERIC_TILED = 2,  /* fused row-tile kernel: TMA-fed, warp-specialised, shared-memory stage,
                                 halo recompute; the tile plan is built on the first call (one sync) */
+    LFEM_NUMERIC_ROWS = 3    /* warp per CSR row, each incident element recomputed per row (cheap
+                                elements); rows longer than 64 columns fall back to V0; the first
+                                call builds the row incidence lists (one sync) */
 } lfem_numeric_variant;
 
 typedef struct lfem_mesh_s* lfem_mesh;

@@ -296,7 +296,7 @@ lfem_status lfem_plan_info(lfem_plan p, int64_t* n_rows, int64_t* nnz, int64_t* 
 
 lfem_status lfem_plan_set_variant(lfem_plan p, lfem_numeric_variant v) {
     if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
-    if (v != LFEM_NUMERIC_AUTO && v != LFEM_NUMERIC_V0 && v != LFEM_NUMERIC_TILED)
+    if (v != LFEM_NUMERIC_AUTO && v != LFEM_NUMERIC_V0 && v != LFEM_NUMERIC_TILED && v != LFEM_NUMERIC_ROWS)
         return lfem_fail(LFEM_ERR_INVALID_ARG, "variant");
     p->variant = v;
     return LFEM_OK;

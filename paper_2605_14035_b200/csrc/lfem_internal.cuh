@@ -90,6 +90,7 @@ struct lfem_plan_s {
     int rhs_tiled = -1;             // -1 not tried, 0 unavailable, 1 tile-local codes built
     int rhs_last_tiled = -1;        // variant of the last lfem_assemble_rhs call (1 fused, 0 two-kernel)
     McfWork mcf;                    // CG / MCF workspace (mcf.cu)
+    int rows_ok = -1;               // ROWS variant (rows.cuh): -1 unknown, 1 every row fits, 0 fall back to V0
 };
 
 // ---------------------------------------------------------------------------

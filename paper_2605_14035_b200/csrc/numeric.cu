@@ -261,6 +261,12 @@ uint64_t g_tab_devices = 0;  // bit per device with uploaded tables
 
 #include "numeric_tiled.cuh"
 
+lfem_status rows_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
+                          double* const vals[3], cudaStream_t s, bool* ok);  // rows.cuh
+
+// AUTO: TILED for triangles, V0 for tetrahedra (measured; ROWS is opt-in)
+static int auto_variant(lfem_plan_s* p) { return tiled_default_variant(p); }
+
 lfem_status upload_reference_tables() {
     int dev = 0;
     LFEM_CUDA(cudaGetDevice(&dev));
@@ -301,8 +307,13 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
                              double* const vals[3], cudaStream_t s) {
     LFEM_TRY(upload_reference_tables());
     const int fam = p->mesh->family;
-    const int variant = p->variant == LFEM_NUMERIC_AUTO ? tiled_default_variant(p) : p->variant;
+    const int variant = p->variant == LFEM_NUMERIC_AUTO ? auto_variant(p) : p->variant;
     if (variant == LFEM_NUMERIC_TILED) return tiled_dispatch(p, kinds, coords, coeff, vals, s);
+    if (variant == LFEM_NUMERIC_ROWS) {
+        bool ok = false;
+        LFEM_TRY(rows_dispatch(p, kinds, coords, coeff, vals, s, &ok));
+        if (ok) return LFEM_OK;  // else: a row longer than the ROWS lanes hold -> V0
+    }
     switch (fam) {
     case FAM_TRI_P1: return dispatch_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return dispatch_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);
@@ -314,8 +325,9 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
 
 int numeric_launch_count(lfem_plan_s* p, unsigned kinds) {
     (void)kinds;
-    const int variant = p->variant == LFEM_NUMERIC_AUTO ? tiled_default_variant(p) : p->variant;
+    const int variant = p->variant == LFEM_NUMERIC_AUTO ? auto_variant(p) : p->variant;
     if (variant == LFEM_NUMERIC_TILED) return tiled_launch_count(p);
+    if (variant == LFEM_NUMERIC_ROWS && p->rows_ok != 0) return p->n_rows > 0 ? 1 : 0;
     return (p->n_local > 0 ? 1 : 0) + (p->nnz > 0 ? 1 : 0);
 }
 
@@ -335,3 +347,4 @@ lfem_status axpby_launch(int64_t n, double ca, const double* a, double cb, const
 }
 
 #include "rhs.cuh"
+#include "rows.cuh"

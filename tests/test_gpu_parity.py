@@ -20,7 +20,7 @@ if not torch.cuda.is_available():  # collected on CPU boxes only with -m gpu
 
 from paper_2605_14035_b200 import lfem  # noqa: E402
 
-VARIANTS = [lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED, lfem.LFEM_NUMERIC_AUTO]
+VARIANTS = [lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED, lfem.LFEM_NUMERIC_AUTO, lfem.LFEM_NUMERIC_ROWS]
 
 
 def _skew(m, seed, eps):
@@ -47,7 +47,7 @@ SMALL = [
 ]
 
 
-@pytest.mark.parametrize("variant", VARIANTS, ids=["v0", "tiled", "auto"])
+@pytest.mark.parametrize("variant", VARIANTS, ids=["v0", "tiled", "auto", "rows"])
 @pytest.mark.parametrize("name,mk", SMALL, ids=[s[0] for s in SMALL])
 def test_parity_full(name, mk, variant):
     m = mk()
@@ -72,7 +72,8 @@ def test_C2_full_parity():
 def test_determinism_and_variant_bitwise():
     m = li.make_config("C5", level_override=5)
     outs = []
-    for variant in (lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED, lfem.LFEM_NUMERIC_AUTO, lfem.LFEM_NUMERIC_AUTO):
+    for variant in (lfem.LFEM_NUMERIC_V0, lfem.LFEM_NUMERIC_TILED, lfem.LFEM_NUMERIC_AUTO, lfem.LFEM_NUMERIC_AUTO,
+                    lfem.LFEM_NUMERIC_ROWS):
         _, rp, ci, vals = gpu_assemble(m, ("M", "A", "Aa"), variant=variant)
         outs.append(vals)
     for o in outs[1:]:
@@ -336,3 +337,19 @@ def test_unreferenced_nodes_give_empty_rows(variant):
     assert worst <= TOL
     assert np.all(np.diff(rp)[unused] == 0)
 
+
+
+@pytest.mark.parametrize("mk", [lambda: li.make_config("C4P1", level_override=12),
+                                lambda: li.perturb(li.sphere_mesh(4, 1), 3, 0.01),
+                                lambda: li.make_config("C4", level_override=4)], ids=["tet1", "tri1", "tet2"])
+def test_rows_variant_bitwise(mk):
+    """ROWS (warp per row, elements recomputed per row) == V0 bit for bit (same element code, same
+    ascending-element order per slot); P2 tets with rows > 64 columns fall back to V0."""
+    m = mk()
+    u = li.random_field(m, 2)
+    _, _, _, a = gpu_assemble(m, ("M", "A", "Aa"), coeff=u, variant=lfem.LFEM_NUMERIC_V0)
+    plan, _, _, b = gpu_assemble(m, ("M", "A", "Aa"), coeff=u, variant=lfem.LFEM_NUMERIC_ROWS)
+    for k in ("M", "A", "Aa"):
+        assert np.array_equal(a[k], b[k]), k
+    if m.order == 1:
+        assert lfem.lfem_numeric_launches(plan, 7) == 1
