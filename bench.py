@@ -360,6 +360,11 @@ def run_rhs(args):
                "d2h_bytes_per_step": int(m.n_nodes * nc * 8), "api": "lfem_assemble_rhs (+ pinned H2D/D2H copies)",
                "steps": ke}
 
+    # verification (untimed): per-component sums of the owned rows, all-reduced over the ranks
+    vsum = out.sum(dim=1).double()
+    if world > 1:
+        dist.all_reduce(vsum)
+    verify = {"component_sums": [float(x) for x in vsum.cpu()]}
     hbm, peak_src = peaks()
     step_kernel_ms = sum(v[0] for v in prof.values()) / max(1, nprof)
     achieved = alg / (step_kernel_ms * 1e-3) / 1e9
@@ -399,7 +404,7 @@ def run_rhs(args):
                                  "inputs+outputs > L2 (126 MB); no flush"},
                 "first_call_ms": first_ms, "generate_s": gen_s,
                 "gpu_launches": lfem.lfem_rhs_launches(plan, k) * args.steps,
-                "roofline": roofline, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
+                "roofline": roofline, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "verify": verify}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

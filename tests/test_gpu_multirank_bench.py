@@ -53,3 +53,17 @@ def test_two_ranks_match_one(cfg):
         assert abs(a - b) <= 1e-12 * max(1.0, abs(a)), (k, a, b)
     if "A" in two["config"]["kinds"]:  # trace identity sum_k x_k^T A x_k = 2 * area (surface, tr P = 2)
         assert abs(two["verify"]["trace_xAx"] - 2 * two["verify"]["one_M_one"]) <= 1e-9 * two["verify"]["one_M_one"]
+
+
+def test_two_ranks_rhs_match_one():
+    """bench.py --rhs kll over two row-block ranks: the all-reduced component sums equal one rank's."""
+    env = dict(os.environ)
+    base = [sys.executable, "bench.py", "--config", "C2", "--rhs", "kll", "--steps", "3", "--warmup", "3",
+            "--no-cpu-baseline", "--no-e2e"]
+    one = _run(base + ["--gpus", "1"], env)
+    env2 = dict(env, LFEM_BENCH_DEVICE="0", LFEM_BENCH_BACKEND="gloo")
+    two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                "--master-addr", "127.0.0.1", "--master-port", str(_port())] + base[1:] + ["--gpus", "2"], env2)
+    assert two["n_gpus"] == 2 and two["gpu_launches"] > 0 and two["value"] > 0
+    for a, b in zip(one["verify"]["component_sums"], two["verify"]["component_sums"]):
+        assert abs(a - b) <= 1e-12 * max(1.0, abs(a)), (a, b)
