@@ -29,10 +29,13 @@ constexpr int RHS_THREADS = 128;
 
 template <int KIND> struct RhsInfo { static constexpr int NC = KIND == LFEM_RHS_KLL ? 4 : 1; };
 
-// minimum resident CTAs per SM (register caps) of the two-kernel element kernel and of the fused kernel
+// minimum resident CTAs per SM (register caps) of the two-kernel element kernel (measured: 3 for the
+// P2 triangle KLL kernel, 4 for the P2 tetrahedron load kernel) and of the fused kernel
 #ifndef LFEM_RHS_MINB
 #define LFEM_RHS_MINB 3
 #endif
+template <int F> struct RhsMinb { static constexpr int V = LFEM_RHS_MINB; };
+template <> struct RhsMinb<FAM_TET_P2> { static constexpr int V = LFEM_RHS_MINB + 1; };
 #ifndef LFEM_RHS_TMINB
 #define LFEM_RHS_TMINB 2
 #endif
@@ -133,7 +136,7 @@ __device__ __forceinline__ bool rhs_local(int64_t le, const int32_t* __restrict_
 }
 
 template <int F, int KIND>
-__global__ void __launch_bounds__(RHS_THREADS, LFEM_RHS_MINB)
+__global__ void __launch_bounds__(RHS_THREADS, RhsMinb<F>::V)
 k_rhs_elem(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __restrict__ elem_list,
            const double* __restrict__ coords, const double* __restrict__ u, int64_t n_nodes,
            double* __restrict__ stage, int* __restrict__ err) {
