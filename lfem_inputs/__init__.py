@@ -119,6 +119,7 @@ QUAD_TRI3_DEG2 = 1
 QUAD_TRI6_DEG4 = 2
 QUAD_TET4_DEG2 = 3
 QUAD_TET11_DEG4 = 4
+QUAD_TRI16_DEG8 = 5  # Dunavant degree 8 (the paper's load-vector rule)
 
 
 @dataclass

@@ -64,7 +64,7 @@
 namespace {
 
 enum { SURFACE_TRI = 0, BULK_TET = 1 };
-enum { Q_DEFAULT = 0, Q_TRI3_DEG2 = 1, Q_TRI6_DEG4 = 2, Q_TET4_DEG2 = 3, Q_TET11_DEG4 = 4 };
+enum { Q_DEFAULT = 0, Q_TRI3_DEG2 = 1, Q_TRI6_DEG4 = 2, Q_TET4_DEG2 = 3, Q_TET11_DEG4 = 4, Q_TRI16_DEG8 = 5 };
 enum { K_MASS = 1, K_STIFF = 2, K_STIFF_COEF = 4 };
 enum { OK = 0, ERR_INVALID_ARG = 1, ERR_UNSUPPORTED = 2, ERR_INDEX = 3, ERR_DEGENERATE = 4 };
 
@@ -122,6 +122,21 @@ bool make_rule(int quad, std::vector<QPoint>& r) {
         const double b = 0.09157621350977074346, wb = 0.10995174365532186764 / 2.0;
         add_orbit3(r, a, a, 1.0 - 2.0 * a, wa);
         add_orbit3(r, b, b, 1.0 - 2.0 * b, wb);
+        return true;
+    }
+    case Q_TRI16_DEG8: {
+        // Dunavant's 16-point degree-8 rule (the paper's load-vector rule; SURVEY
+        // §8(f) N2): centroid, three (a, a, 1-2a) orbits, one (a, b, c) orbit; weights for area
+        // 1/2.  Constants solved here from the degree-8 moment equations (40 digits) and pinned
+        // by the exactness test (exact to degree 8, not 9).
+        add_orbit3(r, 1.0 / 3.0, 1.0 / 3.0, 1.0 / 3.0, 0.07215780383889358412554556);
+        const double a1 = 0.4592925882927231560288155, a2 = 0.1705693077517602066222935,
+                     a3 = 0.05054722831703097545842355;
+        add_orbit3(r, a1, a1, 1.0 - 2.0 * a1, 0.04754581713364231239694805);
+        add_orbit3(r, a2, a2, 1.0 - 2.0 * a2, 0.05160868526735912514089578);
+        add_orbit3(r, a3, a3, 1.0 - 2.0 * a3, 0.01622924881159904015546296);
+        const double a4 = 0.008394777409957605337213835, b4 = 0.2631128296346381134217858;
+        add_orbit3(r, a4, b4, 1.0 - a4 - b4, 0.01361515708721749713242235);
         return true;
     }
     case Q_TET4_DEG2: {
@@ -212,7 +227,7 @@ bool make_ref(int domain, int order, int quad, Ref& R) {
         if (domain == SURFACE_TRI) quad = (order == 1) ? Q_TRI3_DEG2 : Q_TRI6_DEG4;
         else quad = (order == 1) ? Q_TET4_DEG2 : Q_TET11_DEG4;
     }
-    if (domain == SURFACE_TRI && quad != Q_TRI3_DEG2 && quad != Q_TRI6_DEG4) return false;
+    if (domain == SURFACE_TRI && quad != Q_TRI3_DEG2 && quad != Q_TRI6_DEG4 && quad != Q_TRI16_DEG8) return false;
     if (domain == BULK_TET && quad != Q_TET4_DEG2 && quad != Q_TET11_DEG4) return false;
     R.domain = domain;
     R.order = order;
@@ -436,7 +451,7 @@ void oracle_free(oracle_csr* c) {
 int oracle_nref(int domain, int order) { return nref_of(domain, order); }
 
 // Quadrature rule as used by the oracle (for the exactness pins).
-int oracle_rule(int quad, int* nq, double* lam /* 11 x 4 */, double* w /* 11 */) {
+int oracle_rule(int quad, int* nq, double* lam /* 16 x 4 */, double* w /* 16 */) {
     std::vector<QPoint> r;
     if (!make_rule(quad, r)) return ERR_UNSUPPORTED;
     *nq = (int)r.size();

@@ -16,7 +16,7 @@ import pytest
 
 import oracle
 from lfem_inputs import (BULK_TET, QUAD_TET11_DEG4, QUAD_TET4_DEG2, QUAD_TRI3_DEG2,
-                         QUAD_TRI6_DEG4, SURFACE_TRI)
+                         QUAD_TRI6_DEG4, QUAD_TRI16_DEG8, SURFACE_TRI)
 
 # reference nodes in barycentric coordinates, local order of reading G26
 TRI_P2_NODES = [(1, 0, 0), (0, 1, 0), (0, 0, 1), (.5, .5, 0), (0, .5, .5), (.5, 0, .5)]
@@ -78,7 +78,7 @@ def _exact_tet(a, b, c):
     return Fraction(math.factorial(a) * math.factorial(b) * math.factorial(c), math.factorial(a + b + c + 3))
 
 
-@pytest.mark.parametrize("quad,deg,npts", [(QUAD_TRI3_DEG2, 2, 3), (QUAD_TRI6_DEG4, 4, 6)])
+@pytest.mark.parametrize("quad,deg,npts", [(QUAD_TRI3_DEG2, 2, 3), (QUAD_TRI6_DEG4, 4, 6), (QUAD_TRI16_DEG8, 8, 16)])
 def test_triangle_rule_exactness(quad, deg, npts):
     lam, w = oracle.rule(quad)
     assert lam.shape[0] == npts

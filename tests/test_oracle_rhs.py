@@ -261,3 +261,28 @@ def test_abs_scale_is_the_value_for_nonnegative_terms():
     f2 = li.random_field(m2, 4)
     b2, babs2 = oracle.assemble_rhs_rows(m2, f2[None, :], "load", with_abs=True)
     assert np.all(babs2 >= np.abs(b2)) and np.any(babs2 > 2 * np.abs(b2))
+
+
+def test_load_with_dunavant8_on_sphere():
+    """The paper's load-vector rule (Dunavant degree 8): on flat P2 elements f_h phi_j has
+    degree 4, so the 6-point and 16-point rules agree to rounding; on the curved sphere they differ
+    by the rule error only (small), and the sum of b over f == 1 is the area to rule accuracy."""
+    m6 = li.table12_mesh()
+    m16 = li.Mesh(m6.domain, m6.order, m6.coords, m6.conn, li.QUAD_TRI16_DEG8)
+    f = np.array([0.3, -1.0, 2.0, 0.5, 0.1, -0.7, 1.1, 0.0, 0.9])[None, :]
+    b6 = oracle.assemble_rhs_rows(m6, f, "load")
+    b16 = oracle.assemble_rhs_rows(m16, f, "load")
+    # table12 has curved edges (nodes 6, 9 on the circle): only the sum over f == 1 is exact-polynomial
+    s16 = oracle.assemble_rhs_rows(m16, np.ones((1, 9)), "load").sum()
+    assert abs(s16 - (1.0 + 4.0 / 3.0 * (math.sqrt(2.0) - 1.0))) < 1e-14
+    p = plane_mesh(2, 2)
+    fp = li.random_field(p, 3)[None, :]
+    a6 = oracle.assemble_rhs_rows(p, fp, "load")
+    a16 = oracle.assemble_rhs_rows(li.Mesh(p.domain, 2, p.coords, p.conn, li.QUAD_TRI16_DEG8), fp, "load")
+    assert np.allclose(a6, a16, rtol=0, atol=1e-15)
+    s = li.sphere_mesh(2, 2)
+    fs = li.random_field(s, 4)[None, :]
+    c6 = oracle.assemble_rhs_rows(s, fs, "load")
+    c16 = oracle.assemble_rhs_rows(li.Mesh(s.domain, 2, s.coords, s.conn, li.QUAD_TRI16_DEG8), fs, "load")
+    assert 0 < np.max(np.abs(c6 - c16)) < 1e-3 * np.max(np.abs(c16))
+    assert b6.shape == b16.shape
