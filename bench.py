@@ -65,10 +65,18 @@ def algorithmic_bytes(name, n_elems, nref, n_nodes, nnz, kinds, has_coeff):
     return b
 
 
+QUAD8 = False  # --quad8: P2 triangle configs with Dunavant's 16-point degree-8 rule
+
+
 def build_mesh(name):
     import lfem_inputs as li
     t0 = time.time()
     m = li.make_config(name)
+    if QUAD8:
+        if not (m.domain == li.SURFACE_TRI and m.order == 2):
+            raise SystemExit("--quad8 applies to P2 triangle configs (C2, C5)")
+        m.quad = li.QUAD_TRI16_DEG8
+        m.extra["quad8"] = True
     return m, time.time() - t0
 
 
@@ -398,7 +406,7 @@ def run_rhs(args):
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
                 "config": {"workload": f"{name} mesh ({m.n_elems} elements, {m.n_nodes} nodes), {kind} right-hand "
-                                       f"side ({nc} components)", "rhs": kind, "parallelism": f"row-blocks x{world}",
+                                       f"side ({nc} components)" + (", Dunavant-8 rule" if QUAD8 else ""), "rhs": kind, "parallelism": f"row-blocks x{world}",
                            "variant": args.variant,
                            "l2": "flushed (256 MiB write) between steps" if flush else
                                  "inputs+outputs > L2 (126 MB); no flush"},
@@ -895,7 +903,8 @@ def run_lfem(args):
             "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
-            "config": {"workload": f"{name}: {CONFIG_DESC[name]}", "kinds": list(kinds), "n_elems": n_elems,
+            "config": {"workload": f"{name}: {CONFIG_DESC[name]}" + (" [Dunavant-8 rule, 16 points]" if QUAD8 else ""),
+                       "kinds": list(kinds), "n_elems": n_elems,
                        "n_nodes": n_nodes, "nnz": nnz_total, "parallelism": f"row-blocks x{world}",
                        "l2": "flushed (256 MiB write) between steps" if flush else
                              "inputs+outputs > L2 (126 MB); no flush", "variant": args.variant},
@@ -933,9 +942,13 @@ def main():
                     help="time the surface Poisson pipeline (SURVEY §8(f) N4) at the config's icosphere level")
     ap.add_argument("--mcf", action="store_true",
                     help="time Dziuk MCF steps (SURVEY §8(f) N3) on the paper's surface at the config's level")
+    ap.add_argument("--quad8", action="store_true",
+                    help="P2 triangle configs with Dunavant's 16-point degree-8 rule (the paper's load-vector rule)")
     ap.add_argument("--rhs", default=None, choices=["load", "kll"],
                     help="time the right-hand side (SURVEY §8(f) N1) instead of the matrices")
     args = ap.parse_args()
+    global QUAD8
+    QUAD8 = args.quad8
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3

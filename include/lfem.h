@@ -88,7 +88,9 @@ typedef enum {
     LFEM_QUAD_TRI3_DEG2 = 1,  /* 3 points, permutations of (2/3,1/6,1/6), w = 1/6 */
     LFEM_QUAD_TRI6_DEG4 = 2,  /* 6-point symmetric degree-4 rule */
     LFEM_QUAD_TET4_DEG2 = 3,  /* 4-point degree-2 rule */
-    LFEM_QUAD_TET11_DEG4 = 4  /* Keast 11-point degree-4 rule (negative centroid weight) */
+    LFEM_QUAD_TET11_DEG4 = 4, /* Keast 11-point degree-4 rule (negative centroid weight) */
+    LFEM_QUAD_TRI16_DEG8 = 5  /* Dunavant 16-point degree-8 rule, P2 triangles only (the paper's
+                                 load-vector rule) */
 } lfem_quad;
 
 /* 'kinds' bitmask of lfem_assemble_numeric; vals[] index = bit position. */

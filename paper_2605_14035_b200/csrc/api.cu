@@ -196,17 +196,18 @@ lfem_status lfem_mesh_create(lfem_domain dom, int order, lfem_quad quad, int64_t
         else q = order == 1 ? LFEM_QUAD_TET4_DEG2 : LFEM_QUAD_TET11_DEG4;
     }
     // each family runs with the rule its constant tables were built for
-    const int fam = family_of(dom, order);
-    const int want[4] = {LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4, LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4};
+    const int fam = family_of(dom, order, q);
+    const int want[5] = {LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4, LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4,
+                         LFEM_QUAD_TRI16_DEG8};
     if (q != want[fam])
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "quadrature rule not available for this (domain, order)");
     if (n_nodes < 0 || n_elems < 0 || n_nodes >= INT_MAX || n_elems >= INT_MAX)
         return lfem_fail(LFEM_ERR_INVALID_ARG, "n_nodes / n_elems out of range");
     if ((n_nodes > 0 && !coords) || (n_elems > 0 && !conn))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "coords / conn is NULL");
-    static const int nrefs[4] = {3, 6, 4, 10};
-    static const int nqs[4] = {3, 6, 4, 11};
-    static const int nsyms[4] = {6, 21, 10, 55};
+    static const int nrefs[5] = {3, 6, 4, 10, 6};
+    static const int nqs[5] = {3, 6, 4, 11, 16};
+    static const int nsyms[5] = {6, 21, 10, 55, 21};
     lfem_mesh_s* m = new (std::nothrow) lfem_mesh_s();
     if (!m) return lfem_fail(LFEM_ERR_NOMEM, "host allocation");
     m->domain = dom;

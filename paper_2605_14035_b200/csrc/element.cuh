@@ -109,6 +109,7 @@ struct Shape {
 template <int F> struct FamShape;
 template <> struct FamShape<FAM_TRI_P1> { using S = Shape<2, 1>; };
 template <> struct FamShape<FAM_TRI_P2> { using S = Shape<2, 2>; };
+template <> struct FamShape<FAM_TRI_P2_Q16> { using S = Shape<2, 2>; };
 template <> struct FamShape<FAM_TET_P1> { using S = Shape<3, 1>; };
 template <> struct FamShape<FAM_TET_P2> { using S = Shape<3, 2>; };
 
@@ -141,9 +142,9 @@ __device__ __forceinline__ double rcp_nr(double x) {
 
 // reference coordinates of the quadrature points (constant memory)
 struct QuadXi {
-    double xi[11][3];
+    double xi[16][3];
 };
-__constant__ QuadXi c_xi[4];
+__constant__ QuadXi c_xi[5];
 
 enum Kind { KIND_M = 0, KIND_A = 1, KIND_AA = 2 };
 

@@ -129,6 +129,7 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 template <int F> struct TileCfg;
 template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_P1_RU, MINB = 1, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
 template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = LFEM_P2_EPT, RU = LFEM_RU, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
+template <> struct TileCfg<FAM_TRI_P2_Q16> : TileCfg<FAM_TRI_P2> {};
 template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
 
@@ -649,7 +650,7 @@ lfem_status tiled_kinds(lfem_plan_s* p, unsigned kinds, const double* coords, co
 
 inline int tiled_default_variant(lfem_plan_s* p) {
     const int f = p->mesh->family;
-    return (f == FAM_TRI_P1 || f == FAM_TRI_P2) ? LFEM_NUMERIC_TILED : LFEM_NUMERIC_V0;
+    return (f == FAM_TRI_P1 || f == FAM_TRI_P2 || f == FAM_TRI_P2_Q16) ? LFEM_NUMERIC_TILED : LFEM_NUMERIC_V0;
 }
 
 inline lfem_status tiled_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
@@ -657,6 +658,7 @@ inline lfem_status tiled_dispatch(lfem_plan_s* p, unsigned kinds, const double* 
     switch (p->mesh->family) {
     case FAM_TRI_P1: return tiled_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return tiled_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);
+    case FAM_TRI_P2_Q16: return tiled_kinds<FAM_TRI_P2_Q16>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P1: return tiled_kinds<FAM_TET_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P2: return tiled_kinds<FAM_TET_P2>(p, kinds, coords, coeff, vals, s);
     }

@@ -36,20 +36,22 @@ __constant__ RefTab<FAM_TRI_P1> c_tab_tri1;
 __constant__ RefTab<FAM_TRI_P2> c_tab_tri2;
 __constant__ RefTab<FAM_TET_P1> c_tab_tet1;
 __constant__ RefTab<FAM_TET_P2> c_tab_tet2;
+__constant__ RefTab<FAM_TRI_P2_Q16> c_tab_tri2q;
 
 template <int F> __device__ __forceinline__ const RefTab<F>& tab();
 template <> __device__ __forceinline__ const RefTab<FAM_TRI_P1>& tab<FAM_TRI_P1>() { return c_tab_tri1; }
 template <> __device__ __forceinline__ const RefTab<FAM_TRI_P2>& tab<FAM_TRI_P2>() { return c_tab_tri2; }
 template <> __device__ __forceinline__ const RefTab<FAM_TET_P1>& tab<FAM_TET_P1>() { return c_tab_tet1; }
 template <> __device__ __forceinline__ const RefTab<FAM_TET_P2>& tab<FAM_TET_P2>() { return c_tab_tet2; }
+template <> __device__ __forceinline__ const RefTab<FAM_TRI_P2_Q16>& tab<FAM_TRI_P2_Q16>() { return c_tab_tri2q; }
 
 namespace refhost {
 
 // quadrature points in reference coordinates xi (d = 2: (xi1, xi2); d = 3)
 struct Rule {
     int nq;
-    double xi[11][3];
-    double w[11];
+    double xi[16][3];
+    double w[16];
 };
 
 inline Rule rule_tri3() {
@@ -73,6 +75,37 @@ inline Rule rule_tri6() {
         r.xi[q][1] = P[q][1];
         r.w[q] = q < 3 ? wa : wb;
     }
+    return r;
+}
+
+// Dunavant's 16-point degree-8 rule (weights for area 1/2): centroid, three (a, a, 1-2a)
+// orbits, one (a, b, c) orbit -- constants of the published rule, 25 digits
+inline Rule rule_tri16() {
+    Rule r{};
+    r.nq = 0;
+    auto add = [&r](double l1, double l2, double w) {  // xi = (lambda_2, lambda_3)
+        r.xi[r.nq][0] = l1;
+        r.xi[r.nq][1] = l2;
+        r.w[r.nq] = w;
+        ++r.nq;
+    };
+    add(1.0 / 3.0, 1.0 / 3.0, 0.07215780383889358412554556);
+    const double A[3] = {0.4592925882927231560288155, 0.1705693077517602066222935, 0.05054722831703097545842355};
+    const double W[3] = {0.04754581713364231239694805, 0.05160868526735912514089578, 0.01622924881159904015546296};
+    for (int o = 0; o < 3; ++o) {
+        const double a = A[o], c = 1.0 - 2.0 * a;
+        add(a, a, W[o]);
+        add(c, a, W[o]);
+        add(a, c, W[o]);
+    }
+    const double a4 = 0.008394777409957605337213835, b4 = 0.2631128296346381134217858, c4 = 1.0 - a4 - b4;
+    const double w4 = 0.01361515708721749713242235;
+    add(a4, b4, w4);
+    add(b4, a4, w4);
+    add(a4, c4, w4);
+    add(c4, a4, w4);
+    add(b4, c4, w4);
+    add(c4, b4, w4);
     return r;
 }
 

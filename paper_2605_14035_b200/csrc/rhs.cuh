@@ -472,6 +472,9 @@ lfem_status rhs_dispatch(lfem_plan_s* p, int kind, const double* coords, const d
     case FAM_TRI_P2:
         return kll ? run_rhs<FAM_TRI_P2, LFEM_RHS_KLL>(p, coords, u, out, s)
                    : run_rhs<FAM_TRI_P2, LFEM_RHS_LOAD>(p, coords, u, out, s);
+    case FAM_TRI_P2_Q16:
+        return kll ? run_rhs<FAM_TRI_P2_Q16, LFEM_RHS_KLL>(p, coords, u, out, s)
+                   : run_rhs<FAM_TRI_P2_Q16, LFEM_RHS_LOAD>(p, coords, u, out, s);
     case FAM_TET_P1:
         if (kll) break;
         return run_rhs<FAM_TET_P1, LFEM_RHS_LOAD>(p, coords, u, out, s);

@@ -182,6 +182,7 @@ lfem_status rows_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, 
     switch (p->mesh->family) {
     case FAM_TRI_P1: return rows_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return rows_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);
+    case FAM_TRI_P2_Q16: return rows_kinds<FAM_TRI_P2_Q16>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P1: return rows_kinds<FAM_TET_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P2: return rows_kinds<FAM_TET_P2>(p, kinds, coords, coeff, vals, s);
     }

@@ -27,6 +27,11 @@ def _skew(m, seed, eps):
     return li.perturb(m, seed, eps)
 
 
+def _q16(m):
+    """The same mesh with Dunavant's 16-point degree-8 rule."""
+    return li.Mesh(m.domain, m.order, m.coords, m.conn, li.QUAD_TRI16_DEG8, m.coeff)
+
+
 SMALL = [
     ("tri1_single", lambda: li.single_triangle([[0, 0, 0], [1, 0, 0], [0.2, 0.9, 0.3]], 1)),
     ("tri2_single", lambda: li.single_triangle([[0, 0, 0], [1, 0, 0], [0.2, 0.9, 0.3]], 2)),
@@ -44,6 +49,8 @@ SMALL = [
     ("C4_n5", lambda: li.make_config("C4", level_override=5)),
     ("C4P1_n6", lambda: li.make_config("C4P1", level_override=6)),
     ("C5_L4", lambda: li.make_config("C5", level_override=4)),
+    ("sphere2_L3_skew_q16", lambda: _q16(_skew(li.sphere_mesh(3, 2), 3, 0.01))),
+    ("C5_L4_q16", lambda: _q16(li.make_config("C5", level_override=4))),
 ]
 
 

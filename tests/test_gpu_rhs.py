@@ -55,6 +55,8 @@ SURF = [
     ("sphere2_L3_skew", lambda: li.perturb(li.sphere_mesh(3, 2), 3, 0.01)),
     ("sphere2_L4_natural", lambda: li.sphere_mesh(4, 2, sfc=False)),
     ("C5_L5", lambda: li.make_config("C5", level_override=5)),
+    ("sphere2_L3_q16", lambda: li.Mesh(li.SURFACE_TRI, 2, li.sphere_mesh(3, 2).coords, li.sphere_mesh(3, 2).conn,
+                                       li.QUAD_TRI16_DEG8)),
 ]
 BULK = [
     ("cube1_n3", lambda: li.cube_mesh(3, 1, displace_seed=1)),
