@@ -160,11 +160,16 @@ struct Elem {
     // P1 surface: J is constant per element, so the geometry is det*r = mu and
     // r adj(G) (r = 1/mu), the quadrature weights are applied on the fly.
     static constexpr bool P1S = (D == 2 && N == 3);
+    // Many-point surface rules (Dunavant-8, 16 points): geometry() accumulates the stiffness
+    // moments itself instead of keeping K per point (52 instead of 80 live doubles per element;
+    // the same fma sequence in ascending q, so the same bits as forming them in stiffness()).
+    static constexpr bool MOMG = (D == 2) && !P1S && NQ > 8;
     struct Geo {
         double mu1, ka[3];  // P1 surface only
         double wmu[NQ];
-        double k11[D == 2 ? NQ : 1], k12[D == 2 ? NQ : 1], k22[D == 2 ? NQ : 1];
-        double aq[NQ];
+        double k11[D == 2 && !MOMG ? NQ : 1], k12[D == 2 && !MOMG ? NQ : 1], k22[D == 2 && !MOMG ? NQ : 1];
+        double aq[MOMG ? 1 : NQ];
+        double mom[MOMG ? 2 : 1][3][6];  // MOMG: moments of K (A) and of a K (A_a)
         double J0[3][D], J1[3][D][D];  // bulk only (unused on surfaces)
     };
 
@@ -256,6 +261,14 @@ struct Elem {
                 }
             }
         } else {
+            if constexpr (MOMG) {
+#pragma unroll
+                for (int m = 0; m < 2; ++m)
+#pragma unroll
+                    for (int c = 0; c < 3; ++c)
+#pragma unroll
+                        for (int al = 0; al < 6; ++al) g.mom[m][c][al] = 0.0;
+            }
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 double J[3][D];
@@ -269,20 +282,42 @@ struct Elem {
                     const double r = rsqrt_nr(det);
                     g.wmu[q] = T.w[q] * (det * r);
                     const double c = T.w[q] * r;
-                    g.k11[D == 2 ? q : 0] = c * g22;
-                    g.k12[D == 2 ? q : 0] = -c * g12;
-                    g.k22[D == 2 ? q : 0] = c * g11;
+                    if constexpr (MOMG) {
+                        constexpr typename S::MTab MT = S::mtab();
+                        double kc[3] = {c * g22, -c * g12, c * g11};
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                            for (int al = 0; al < 6; ++al)
+                                if (MT.used[cc][al]) g.mom[0][cc][al] = fma(kc[cc], T.mono[q][al], g.mom[0][cc][al]);
+                        if (COEF) {
+                            double u = 0.0;
+#pragma unroll
+                            for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
+                            const double aq = fma(u, u, 1.0);
+#pragma unroll
+                            for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                                for (int al = 0; al < 6; ++al)
+                                    if (MT.used[cc][al])
+                                        g.mom[1][cc][al] = fma(aq * kc[cc], T.mono[q][al], g.mom[1][cc][al]);
+                        }
+                    } else {
+                        g.k11[D == 2 && !MOMG ? q : 0] = c * g22;
+                        g.k12[D == 2 && !MOMG ? q : 0] = -c * g12;
+                        g.k22[D == 2 && !MOMG ? q : 0] = c * g11;
+                    }
                 } else {
                     double C[3][3];
                     const double adet = fabs(cof(J, C));
                     ok &= (adet > 0.0) & (adet < INFINITY);
                     g.wmu[q] = T.w[q] * adet;
                 }
-                if (COEF) {
+                if (COEF && !MOMG) {
                     double u = 0.0;
 #pragma unroll
                     for (int j = 0; j < N; ++j) u = fma(U[j], T.phi[q][j], u);
-                    g.aq[q] = fma(u, u, 1.0);
+                    g.aq[MOMG ? 0 : q] = fma(u, u, 1.0);
                 }
             }
             if constexpr (D == 3) {
@@ -336,21 +371,24 @@ struct Elem {
 #pragma unroll
             for (int c = 0; c < 3; ++c)
 #pragma unroll
-                for (int al = 0; al < 6; ++al) mom[c][al] = 0.0;
+                for (int al = 0; al < 6; ++al) mom[c][al] = MOMG ? g.mom[MOMG && COEF ? 1 : 0][c][al] : 0.0;
+            if constexpr (!MOMG) {
 #pragma unroll
-            for (int q = 0; q < NQ; ++q) {
-                double kc[3] = {g.k11[D == 2 ? q : 0], g.k12[D == 2 ? q : 0], g.k22[D == 2 ? q : 0]};
-                if (P1S)
+                for (int q = 0; q < NQ; ++q) {
+                    double kc[3] = {g.k11[D == 2 && !MOMG ? q : 0], g.k12[D == 2 && !MOMG ? q : 0],
+                                    g.k22[D == 2 && !MOMG ? q : 0]};
+                    if (P1S)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) kc[c] = T.w[q] * g.ka[c];
-                if (COEF)
+                        for (int c = 0; c < 3; ++c) kc[c] = T.w[q] * g.ka[c];
+                    if (COEF)
 #pragma unroll
-                    for (int c = 0; c < 3; ++c) kc[c] = g.aq[q] * kc[c];
+                        for (int c = 0; c < 3; ++c) kc[c] = g.aq[MOMG ? 0 : q] * kc[c];
 #pragma unroll
-                for (int c = 0; c < 3; ++c)
+                    for (int c = 0; c < 3; ++c)
 #pragma unroll
-                    for (int al = 0; al < 6; ++al)
-                        if (MT.used[c][al]) mom[c][al] = fma(kc[c], T.mono[q][al], mom[c][al]);
+                        for (int al = 0; al < 6; ++al)
+                            if (MT.used[c][al]) mom[c][al] = fma(kc[c], T.mono[q][al], mom[c][al]);
+                }
             }
 #pragma unroll
             for (int s = 0; s < NS; ++s) {

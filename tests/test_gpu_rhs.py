@@ -210,3 +210,20 @@ def test_rhs_fullsize_sampled(cfg, kind):
     rows = sample_rows(m.n_nodes, 3000, seed=3)
     o, oabs = oracle.assemble_rhs_rows(m, u, kind, rows=rows, with_abs=True)
     check(out[:, torch.as_tensor(rows, device="cuda")].cpu().numpy(), o, oabs)
+
+
+@pytest.mark.parametrize("variant", VARIANTS, ids=["v0", "fused"])
+def test_rhs_empty_row_block_and_tiny_mesh(variant):
+    """Degenerate sizes: an empty owned-row block, a one-row block, and a single element."""
+    m = li.sphere_mesh(2, 2)
+    u = fields(m, "kll")
+    _, out = lfem.assemble_rhs(m, u, "kll", row_begin=7, row_end=7, variant=variant)
+    assert tuple(out.shape) == (4, 0)
+    _, one = lfem.assemble_rhs(m, u, "kll", row_begin=7, row_end=8, variant=variant)
+    o, oabs = oracle.assemble_rhs_rows(m, u, "kll", rows=np.array([7], dtype=np.int64), with_abs=True)
+    check(one.cpu().numpy(), o, oabs)
+    t = li.single_triangle([[0, 0, 0], [1, 0, 0], [0.2, 0.9, 0.3]], 2)
+    ut = fields(t, "load")
+    _, ot = lfem.assemble_rhs(t, ut, "load", variant=variant)
+    o2, oabs2 = oracle.assemble_rhs_rows(t, ut, "load", with_abs=True)
+    check(ot.cpu().numpy(), o2, oabs2)
