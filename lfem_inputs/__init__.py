@@ -120,6 +120,9 @@ QUAD_TRI6_DEG4 = 2
 QUAD_TET4_DEG2 = 3
 QUAD_TET11_DEG4 = 4
 QUAD_TRI16_DEG8 = 5  # Dunavant degree 8 (the paper's load-vector rule)
+QUAD_LINE2_DEG3 = 6  # 2-point Gauss-Legendre (curves)
+QUAD_LINE3_DEG5 = 7  # 3-point Gauss-Legendre
+SURFACE_LINE = 2     # curves in R^3 (Table 4 "surface 1D")
 
 
 @dataclass
@@ -625,3 +628,17 @@ def dziuk_surface(level: int, order: int = 2, sfc: bool = True) -> Mesh:
     x = m.coords
     s = 1.0 + 0.5 * np.sin(2.0 * math.pi * (x[:, 0] + x[:, 1])) * np.cos(0.25 * x[:, 2] * math.pi)
     return _finish(Mesh(m.domain, m.order, s[:, None] * x, m.conn, m.quad))
+
+
+def circle_mesh(n: int, order: int = 1, radius: float = 1.0) -> Mesh:
+    """Unit circle in the z = 0 plane: n vertices, n line elements; P2 inserts each
+    element's midpoint node projected to the circle (nodes: vertices first)."""
+    t = 2.0 * math.pi * np.arange(n) / n
+    v = radius * np.stack([np.cos(t), np.sin(t), np.zeros(n)], axis=1)
+    e = np.stack([np.arange(n), (np.arange(n) + 1) % n], axis=1).astype(np.int32)
+    if order == 1:
+        return _finish(Mesh(SURFACE_LINE, 1, v, e, QUAD_LINE2_DEG3))
+    tm = t + math.pi / n
+    mid = radius * np.stack([np.cos(tm), np.sin(tm), np.zeros(n)], axis=1)
+    conn = np.concatenate([e, (n + np.arange(n))[:, None]], axis=1).astype(np.int32)
+    return _finish(Mesh(SURFACE_LINE, 2, np.vstack([v, mid]), conn, QUAD_LINE3_DEG5))

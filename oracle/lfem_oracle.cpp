@@ -32,6 +32,9 @@
 //      when conn[e,a] is a requested row;
 //   3. the map's (row, col) order is CSR order (explicit zeros kept, G19).
 // Per-slot summation order: ascending element id, then (a, b) (reading G21).
+// Curves (Table 4 P:646-660 "surface 1D"): P1/P2
+// line elements in R^3 with Gauss-Legendre rules; mu = |t| and g = t |t|^-2 dphi,
+// the d = 1 case of the surface formulas.
 //
 // Right-hand sides, for every requested row j:
 //   load:  b_j = sum_{E ∋ j} sum_q w_q mu_E(xi_q) f_h(xi_q) phi_j(xi_q),
@@ -63,8 +66,12 @@
 
 namespace {
 
-enum { SURFACE_TRI = 0, BULK_TET = 1 };
-enum { Q_DEFAULT = 0, Q_TRI3_DEG2 = 1, Q_TRI6_DEG4 = 2, Q_TET4_DEG2 = 3, Q_TET11_DEG4 = 4, Q_TRI16_DEG8 = 5 };
+enum { SURFACE_TRI = 0, BULK_TET = 1, SURFACE_LINE = 2 };
+enum { Q_DEFAULT = 0, Q_TRI3_DEG2 = 1, Q_TRI6_DEG4 = 2, Q_TET4_DEG2 = 3, Q_TET11_DEG4 = 4, Q_TRI16_DEG8 = 5,
+       Q_LINE2_DEG3 = 6, Q_LINE3_DEG5 = 7 };
+
+// dimension of the reference element: curves 1, surfaces 2, bulk 3
+int dim_of(int domain) { return domain == SURFACE_LINE ? 1 : domain == SURFACE_TRI ? 2 : 3; }
 enum { K_MASS = 1, K_STIFF = 2, K_STIFF_COEF = 4 };
 enum { OK = 0, ERR_INVALID_ARG = 1, ERR_UNSUPPORTED = 2, ERR_INDEX = 3, ERR_DEGENERATE = 4 };
 
@@ -139,6 +146,23 @@ bool make_rule(int quad, std::vector<QPoint>& r) {
         add_orbit3(r, a4, b4, 1.0 - a4 - b4, 0.01361515708721749713242235);
         return true;
     }
+    case Q_LINE2_DEG3:
+    case Q_LINE3_DEG5: {
+        // Gauss-Legendre on [0, 1] (curves, N2): lam = (1 - xi, xi), weights sum to 1
+        const bool three = quad == Q_LINE3_DEG5;
+        const double h = three ? 0.5 * std::sqrt(3.0 / 5.0) : 0.5 / std::sqrt(3.0);
+        const double xs[3] = {0.5 - h, 0.5 + h, 0.5};
+        const double ws[3] = {three ? 5.0 / 18.0 : 0.5, three ? 5.0 / 18.0 : 0.5, 4.0 / 9.0};
+        for (int k = 0; k < (three ? 3 : 2); ++k) {
+            QPoint q;
+            q.lam[0] = 1.0 - xs[k];
+            q.lam[1] = xs[k];
+            q.lam[2] = q.lam[3] = 0.0;
+            q.w = ws[k];
+            r.push_back(q);
+        }
+        return true;
+    }
     case Q_TET4_DEG2: {
         const double s5 = std::sqrt(5.0);
         const double al = (5.0 - s5) / 20.0, be = (5.0 + 3.0 * s5) / 20.0;
@@ -179,14 +203,14 @@ double dlam(int k, int m) {
 }
 
 int nref_of(int domain, int order) {
-    const int d = (domain == SURFACE_TRI) ? 2 : 3;
+    const int d = dim_of(domain);
     if (order == 1) return d + 1;
     return (d + 1) * (d + 2) / 2;
 }
 
 // phi[a], grad[a][m] at barycentric point lam
 void basis(int domain, int order, const double* lam, double* phi, double (*grad)[3]) {
-    const int d = (domain == SURFACE_TRI) ? 2 : 3;
+    const int d = dim_of(domain);
     for (int a = 0; a < 10; ++a) { grad[a][0] = grad[a][1] = grad[a][2] = 0.0; }
     if (order == 1) {
         for (int a = 0; a <= d; ++a) {
@@ -199,10 +223,10 @@ void basis(int domain, int order, const double* lam, double* phi, double (*grad)
         phi[a] = lam[a] * (2.0 * lam[a] - 1.0);
         for (int m = 0; m < d; ++m) grad[a][m] = (4.0 * lam[a] - 1.0) * dlam(a, m);
     }
-    const int ne = (d == 2) ? 3 : 6;
+    const int ne = (d == 1) ? 1 : (d == 2) ? 3 : 6;  // curves: one edge (1,2), the midpoint node
     for (int e = 0; e < ne; ++e) {
-        const int i = (d == 2) ? TRI_EDGES[e][0] : TET_EDGES[e][0];
-        const int j = (d == 2) ? TRI_EDGES[e][1] : TET_EDGES[e][1];
+        const int i = (d <= 2) ? TRI_EDGES[e][0] : TET_EDGES[e][0];
+        const int j = (d <= 2) ? TRI_EDGES[e][1] : TET_EDGES[e][1];
         const int a = d + 1 + e;
         phi[a] = 4.0 * lam[i] * lam[j];
         for (int m = 0; m < d; ++m) grad[a][m] = 4.0 * (lam[i] * dlam(j, m) + lam[j] * dlam(i, m));
@@ -221,17 +245,19 @@ struct Ref {
 };
 
 bool make_ref(int domain, int order, int quad, Ref& R) {
-    if (domain != SURFACE_TRI && domain != BULK_TET) return false;
+    if (domain != SURFACE_TRI && domain != BULK_TET && domain != SURFACE_LINE) return false;
     if (order != 1 && order != 2) return false;
     if (quad == Q_DEFAULT) {
-        if (domain == SURFACE_TRI) quad = (order == 1) ? Q_TRI3_DEG2 : Q_TRI6_DEG4;
+        if (domain == SURFACE_LINE) quad = (order == 1) ? Q_LINE2_DEG3 : Q_LINE3_DEG5;
+        else if (domain == SURFACE_TRI) quad = (order == 1) ? Q_TRI3_DEG2 : Q_TRI6_DEG4;
         else quad = (order == 1) ? Q_TET4_DEG2 : Q_TET11_DEG4;
     }
     if (domain == SURFACE_TRI && quad != Q_TRI3_DEG2 && quad != Q_TRI6_DEG4 && quad != Q_TRI16_DEG8) return false;
     if (domain == BULK_TET && quad != Q_TET4_DEG2 && quad != Q_TET11_DEG4) return false;
+    if (domain == SURFACE_LINE && quad != Q_LINE2_DEG3 && quad != Q_LINE3_DEG5) return false;
     R.domain = domain;
     R.order = order;
-    R.d = (domain == SURFACE_TRI) ? 2 : 3;
+    R.d = dim_of(domain);
     R.nref = nref_of(domain, order);
     if (!make_rule(quad, R.rule)) return false;
     R.phi.resize(R.rule.size());
@@ -285,6 +311,16 @@ void jacobian(const Ref& R, const double* X /* nref x 3 */, size_t q, double J[3
 //                independent formulation by the brute-force pin.
 int point_gradients(const Ref& R, const double J[3][3], size_t q, int formulation, double* mu, double g[10][3]) {
     const int n = R.nref, d = R.d;
+    if (d == 1) {
+        // curve: G = |t|^2, mu = |t|, g = t G^{-1} d phi / d xi  (the d = 1 case of J G^{-1} grad)
+        if (formulation != 0) return ERR_UNSUPPORTED;
+        const double G = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+        *mu = std::sqrt(G);
+        if (!(*mu > 0.0) || !std::isfinite(*mu)) return ERR_DEGENERATE;
+        for (int a = 0; a < n; ++a)
+            for (int c = 0; c < 3; ++c) g[a][c] = J[c][0] * (R.grad[q][a][0] / G);
+        return OK;
+    }
     if (d == 2) {
         double G[2][2];
         for (int a = 0; a < 2; ++a)
@@ -464,7 +500,8 @@ int oracle_rule(int quad, int* nq, double* lam /* 16 x 4 */, double* w /* 16 */)
 
 // Basis values / reference gradients at a barycentric point (for the pins).
 int oracle_basis(int domain, int order, const double* lam, double* phi /* 10 */, double* grad /* 10 x 3 */) {
-    if ((domain != SURFACE_TRI && domain != BULK_TET) || (order != 1 && order != 2)) return ERR_UNSUPPORTED;
+    if ((domain != SURFACE_TRI && domain != BULK_TET && domain != SURFACE_LINE) || (order != 1 && order != 2))
+        return ERR_UNSUPPORTED;
     double g[10][3];
     basis(domain, order, lam, phi, g);
     for (int a = 0; a < 10; ++a)
