@@ -39,9 +39,10 @@ CONFIG_DESC = {
     "C4": "P2 Kuhn cube 96^3x6 (5,308,416 tets), displaced, M+A, TET11_DEG4",
     "C5": "P2 icosphere L10 (20,971,520 curved tri, 41,943,042 nodes), SFC order, M+A+A_a, TRI6_DEG4",
     "C4P1": "P1 Kuhn cube 96^3x6 (5,308,416 tets, 912,673 nodes), displaced, M+A, TET4_DEG2 (SURVEY N2)",
+    "CURVE2": "P2 unit circle, 8,388,608 line elements (16,777,216 nodes), M+A, 3-point Gauss (SURVEY N2)",
 }
 FLOP_PER_ELEM = {"C1": 120, "C2": 1780, "C3": 120, "C4": 9600, "C5": 2640,  # SURVEY §8(d).3 model
-                 "C4P1": 700}  # P1 tet: J, cofactors, det per point (4 points) + 2 x 10 entries
+                 "C4P1": 700, "CURVE2": 150}  # P1 tet: J, cofactors, det per point (4 points) + 2 x 10 entries
 
 
 def log(*a):
@@ -930,7 +931,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "C4P1"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "C4P1", "CURVE2"])
     ap.add_argument("--impl", default="lfem", choices=["lfem", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "v0", "tiled", "rows"])
     ap.add_argument("--e2e-steps", type=int, default=5)

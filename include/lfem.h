@@ -78,7 +78,9 @@ typedef enum {
 
 typedef enum {
     LFEM_SURFACE_TRI = 0, /* 2-D triangles embedded in R^3 (§3) */
-    LFEM_BULK_TET = 1     /* 3-D tetrahedra (Remark P:278-281) */
+    LFEM_BULK_TET = 1,    /* 3-D tetrahedra (Remark P:278-281) */
+    LFEM_SURFACE_LINE = 2 /* curves: line elements in R^3 (Table 4 "surface 1D"; SURVEY
+                             §8(f) N2); numeric variant V0, right-hand side LOAD */
 } lfem_domain;
 
 /* Quadrature rules (BASELINE.json configs; readings G6-G9). DEFAULT picks
@@ -89,8 +91,10 @@ typedef enum {
     LFEM_QUAD_TRI6_DEG4 = 2,  /* 6-point symmetric degree-4 rule */
     LFEM_QUAD_TET4_DEG2 = 3,  /* 4-point degree-2 rule */
     LFEM_QUAD_TET11_DEG4 = 4, /* Keast 11-point degree-4 rule (negative centroid weight) */
-    LFEM_QUAD_TRI16_DEG8 = 5  /* Dunavant 16-point degree-8 rule, P2 triangles only (the paper's
+    LFEM_QUAD_TRI16_DEG8 = 5, /* Dunavant 16-point degree-8 rule, P2 triangles only (the paper's
                                  load-vector rule) */
+    LFEM_QUAD_LINE2_DEG3 = 6, /* 2-point Gauss-Legendre (P1 curves) */
+    LFEM_QUAD_LINE3_DEG5 = 7  /* 3-point Gauss-Legendre (P2 curves) */
 } lfem_quad;
 
 /* 'kinds' bitmask of lfem_assemble_numeric; vals[] index = bit position. */

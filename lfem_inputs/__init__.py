@@ -587,6 +587,11 @@ def make_config(name: str, seed: int = 0, level_override: Optional[int] = None) 
         x, t = sfc_reorder(x, t, 4)
         m = Mesh(BULK_TET, 1, x, t, QUAD_TET4_DEG2)
         m.extra["kinds"] = ("M", "A")
+    elif name == "CURVE2":
+        # SURVEY §8(f) N2 curves at scale: the P2 unit circle with 2^23 elements (16.8M nodes)
+        n = (1 << 23) if level_override is None else level_override
+        m = circle_mesh(n, 2)
+        m.extra["kinds"] = ("M", "A")
     elif name == "C5":
         L = 10 if level_override is None else level_override
         v, f = icosphere_p1(L)

@@ -188,26 +188,28 @@ lfem_status lfem_mesh_create(lfem_domain dom, int order, lfem_quad quad, int64_t
     g_err_elem = -1;
     if (!out) return lfem_fail(LFEM_ERR_INVALID_ARG, "out is NULL");
     *out = nullptr;
-    if (dom != LFEM_SURFACE_TRI && dom != LFEM_BULK_TET) return lfem_fail(LFEM_ERR_UNSUPPORTED, "domain");
+    if (dom != LFEM_SURFACE_TRI && dom != LFEM_BULK_TET && dom != LFEM_SURFACE_LINE)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "domain");
     if (order != 1 && order != 2) return lfem_fail(LFEM_ERR_UNSUPPORTED, "order must be 1 or 2");
     int q = quad;
     if (q == LFEM_QUAD_DEFAULT) {
-        if (dom == LFEM_SURFACE_TRI) q = order == 1 ? LFEM_QUAD_TRI3_DEG2 : LFEM_QUAD_TRI6_DEG4;
+        if (dom == LFEM_SURFACE_LINE) q = order == 1 ? LFEM_QUAD_LINE2_DEG3 : LFEM_QUAD_LINE3_DEG5;
+        else if (dom == LFEM_SURFACE_TRI) q = order == 1 ? LFEM_QUAD_TRI3_DEG2 : LFEM_QUAD_TRI6_DEG4;
         else q = order == 1 ? LFEM_QUAD_TET4_DEG2 : LFEM_QUAD_TET11_DEG4;
     }
     // each family runs with the rule its constant tables were built for
     const int fam = family_of(dom, order, q);
-    const int want[5] = {LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4, LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4,
-                         LFEM_QUAD_TRI16_DEG8};
+    const int want[7] = {LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4,  LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4,
+                         LFEM_QUAD_TRI16_DEG8, LFEM_QUAD_LINE2_DEG3, LFEM_QUAD_LINE3_DEG5};
     if (q != want[fam])
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "quadrature rule not available for this (domain, order)");
     if (n_nodes < 0 || n_elems < 0 || n_nodes >= INT_MAX || n_elems >= INT_MAX)
         return lfem_fail(LFEM_ERR_INVALID_ARG, "n_nodes / n_elems out of range");
     if ((n_nodes > 0 && !coords) || (n_elems > 0 && !conn))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "coords / conn is NULL");
-    static const int nrefs[5] = {3, 6, 4, 10, 6};
-    static const int nqs[5] = {3, 6, 4, 11, 16};
-    static const int nsyms[5] = {6, 21, 10, 55, 21};
+    static const int nrefs[7] = {3, 6, 4, 10, 6, 2, 3};
+    static const int nqs[7] = {3, 6, 4, 11, 16, 2, 3};
+    static const int nsyms[7] = {6, 21, 10, 55, 21, 3, 6};
     lfem_mesh_s* m = new (std::nothrow) lfem_mesh_s();
     if (!m) return lfem_fail(LFEM_ERR_NOMEM, "host allocation");
     m->domain = dom;

@@ -37,7 +37,7 @@
 template <int D, int ORDER>
 struct Shape {
     static constexpr int NV = D + 1;
-    static constexpr int N = ORDER == 1 ? NV : NV + (D == 2 ? 3 : 6);
+    static constexpr int N = ORDER == 1 ? NV : NV + (D == 1 ? 1 : D == 2 ? 3 : 6);
     __host__ __device__ static constexpr int g(int k, int m) { return k == 0 ? -1 : (k == m + 1 ? 1 : 0); }
     __host__ __device__ static constexpr int c(int k) { return k == 0 ? 1 : 0; }
     __host__ __device__ static constexpr int ei(int e) {
@@ -110,6 +110,8 @@ template <int F> struct FamShape;
 template <> struct FamShape<FAM_TRI_P1> { using S = Shape<2, 1>; };
 template <> struct FamShape<FAM_TRI_P2> { using S = Shape<2, 2>; };
 template <> struct FamShape<FAM_TRI_P2_Q16> { using S = Shape<2, 2>; };
+template <> struct FamShape<FAM_LINE_P1> { using S = Shape<1, 1>; };
+template <> struct FamShape<FAM_LINE_P2> { using S = Shape<1, 2>; };
 template <> struct FamShape<FAM_TET_P1> { using S = Shape<3, 1>; };
 template <> struct FamShape<FAM_TET_P2> { using S = Shape<3, 2>; };
 
@@ -144,7 +146,7 @@ __device__ __forceinline__ double rcp_nr(double x) {
 struct QuadXi {
     double xi[16][3];
 };
-__constant__ QuadXi c_xi[5];
+__constant__ QuadXi c_xi[7];
 
 enum Kind { KIND_M = 0, KIND_A = 1, KIND_AA = 2 };
 
@@ -167,7 +169,7 @@ struct Elem {
     struct Geo {
         double mu1, ka[3];  // P1 surface only
         double wmu[NQ];
-        double k11[D == 2 && !MOMG ? NQ : 1], k12[D == 2 && !MOMG ? NQ : 1], k22[D == 2 && !MOMG ? NQ : 1];
+        double k11[D <= 2 && !MOMG ? NQ : 1], k12[D == 2 && !MOMG ? NQ : 1], k22[D == 2 && !MOMG ? NQ : 1];
         double aq[MOMG ? 1 : NQ];
         double mom[MOMG ? 2 : 1][3][6];  // MOMG: moments of K (A) and of a K (A_a)
         double J0[3][D], J1[3][D][D];  // bulk only (unused on surfaces)
@@ -273,7 +275,14 @@ struct Elem {
             for (int q = 0; q < NQ; ++q) {
                 double J[3][D];
                 jac_at(J0, J1, q, J);
-                if constexpr (D == 2) {
+                if constexpr (D == 1) {
+                    // curve: G = |t|^2, mu = |t|, K = w / mu (the d = 1 metric form)
+                    const double det = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+                    ok &= (det > 0.0) & (det < INFINITY);
+                    const double r = rsqrt_nr(det);
+                    g.wmu[q] = T.w[q] * (det * r);
+                    g.k11[q] = T.w[q] * r;
+                } else if constexpr (D == 2) {
                     const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
                     const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
                     const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
@@ -357,7 +366,20 @@ struct Elem {
     template <bool COEF, class Sink>
     static __device__ __forceinline__ void stiffness(const Geo& g, Sink& sink) {
         const RefTab<F>& T = tab<F>();
-        if constexpr (D == 2) {
+        if constexpr (D == 1) {
+            // curve: A_loc(a,b) = sum_q (w_q / mu_q) dphi_a dphi_b
+            double acc[NS];
+#pragma unroll
+            for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const double kc = COEF ? g.aq[q] * g.k11[q] : g.k11[q];
+#pragma unroll
+                for (int s = 0; s < NS; ++s) acc[s] = fma(kc, T.gg[q][s][0], acc[s]);
+            }
+#pragma unroll
+            for (int s = 0; s < NS; ++s) sink(s, acc[s]);
+        } else if constexpr (D == 2) {
             // Moment form.  The reference gradients are affine in xi, so
             //   A_loc(a,b) = sum_q sum_c K_q^c (d phi_a d phi_b)_c(xi_q)
             //              = sum_{c, al} MCOEF(a,b,c,al) * mom[c][al],

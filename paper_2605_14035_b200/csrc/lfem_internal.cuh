@@ -11,7 +11,8 @@
 // ---------------------------------------------------------------------------
 // element families
 // ---------------------------------------------------------------------------
-enum Family { FAM_TRI_P1 = 0, FAM_TRI_P2 = 1, FAM_TET_P1 = 2, FAM_TET_P2 = 3, FAM_TRI_P2_Q16 = 4 };
+enum Family { FAM_TRI_P1 = 0, FAM_TRI_P2 = 1, FAM_TET_P1 = 2, FAM_TET_P2 = 3, FAM_TRI_P2_Q16 = 4, FAM_LINE_P1 = 5,
+              FAM_LINE_P2 = 6 };
 
 template <int F> struct FamInfo;
 template <> struct FamInfo<FAM_TRI_P1> { static constexpr int NREF = 3, D = 2, NQ = 3, NSYM = 6; };
@@ -20,6 +21,9 @@ template <> struct FamInfo<FAM_TET_P1> { static constexpr int NREF = 4, D = 3, N
 template <> struct FamInfo<FAM_TET_P2> { static constexpr int NREF = 10, D = 3, NQ = 11, NSYM = 55; };
 // P2 triangles with Dunavant's 16-point degree-8 rule (the paper's load-vector rule)
 template <> struct FamInfo<FAM_TRI_P2_Q16> { static constexpr int NREF = 6, D = 2, NQ = 16, NSYM = 21; };
+// curves: Gauss-Legendre 2 / 3 points
+template <> struct FamInfo<FAM_LINE_P1> { static constexpr int NREF = 2, D = 1, NQ = 2, NSYM = 3; };
+template <> struct FamInfo<FAM_LINE_P2> { static constexpr int NREF = 3, D = 1, NQ = 3, NSYM = 6; };
 
 // index of (a, b), a <= b, in the row-major upper triangle of an n x n matrix
 __host__ __device__ constexpr int sym_index(int n, int a, int b) {
@@ -180,6 +184,7 @@ lfem_status check_conn_launch(const int32_t* conn, int64_t n_elems, int nref, in
                               cudaStream_t s);
 
 inline int family_of(int domain, int order, int quad = LFEM_QUAD_DEFAULT) {
+    if (domain == LFEM_SURFACE_LINE) return order == 1 ? FAM_LINE_P1 : FAM_LINE_P2;
     if (domain == LFEM_SURFACE_TRI && order == 2 && quad == LFEM_QUAD_TRI16_DEG8) return FAM_TRI_P2_Q16;
     if (domain == LFEM_SURFACE_TRI) return order == 1 ? FAM_TRI_P1 : FAM_TRI_P2;
     return order == 1 ? FAM_TET_P1 : FAM_TET_P2;

@@ -277,20 +277,27 @@ lfem_status upload_reference_tables() {
     static RefTab<FAM_TET_P1> t3;
     static RefTab<FAM_TET_P2> t4;
     static RefTab<FAM_TRI_P2_Q16> t5;
+    static RefTab<FAM_LINE_P1> t6;
+    static RefTab<FAM_LINE_P2> t7;
     refhost::fill(t1, refhost::rule_tri3(), 2, 1);
     refhost::fill(t2, refhost::rule_tri6(), 2, 2);
     refhost::fill(t3, refhost::rule_tet4(), 3, 1);
     refhost::fill(t4, refhost::rule_tet11(), 3, 2);
     refhost::fill(t5, refhost::rule_tri16(), 2, 2);
+    refhost::fill(t6, refhost::rule_line(2), 1, 1);
+    refhost::fill(t7, refhost::rule_line(3), 1, 2);
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri1, &t1, sizeof(t1)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri2, &t2, sizeof(t2)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tet1, &t3, sizeof(t3)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tet2, &t4, sizeof(t4)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri2q, &t5, sizeof(t5)));
-    QuadXi xi[5] = {};
-    const refhost::Rule rules[5] = {refhost::rule_tri3(), refhost::rule_tri6(), refhost::rule_tet4(),
-                                    refhost::rule_tet11(), refhost::rule_tri16()};
-    for (int f = 0; f < 5; ++f)
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_line1, &t6, sizeof(t6)));
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_line2, &t7, sizeof(t7)));
+    QuadXi xi[7] = {};
+    const refhost::Rule rules[7] = {refhost::rule_tri3(),  refhost::rule_tri6(),   refhost::rule_tet4(),
+                                    refhost::rule_tet11(), refhost::rule_tri16(),  refhost::rule_line(2),
+                                    refhost::rule_line(3)};
+    for (int f = 0; f < 7; ++f)
         for (int q = 0; q < rules[f].nq; ++q)
             for (int m = 0; m < 3; ++m) xi[f].xi[q][m] = rules[f].xi[q][m];
     LFEM_CUDA(cudaMemcpyToSymbol(c_xi, xi, sizeof(xi)));
@@ -321,6 +328,8 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
     case FAM_TRI_P1: return dispatch_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return dispatch_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2_Q16: return dispatch_kinds<FAM_TRI_P2_Q16>(p, kinds, coords, coeff, vals, s);
+    case FAM_LINE_P1: return dispatch_kinds<FAM_LINE_P1>(p, kinds, coords, coeff, vals, s);
+    case FAM_LINE_P2: return dispatch_kinds<FAM_LINE_P2>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P1: return dispatch_kinds<FAM_TET_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P2: return dispatch_kinds<FAM_TET_P2>(p, kinds, coords, coeff, vals, s);
     }

@@ -655,6 +655,8 @@ inline int tiled_default_variant(lfem_plan_s* p) {
 
 inline lfem_status tiled_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
                                   double* const vals[3], cudaStream_t s) {
+    if (p->mesh->family == FAM_LINE_P1 || p->mesh->family == FAM_LINE_P2)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "the tiled variant has no curve configuration (use V0 / AUTO)");
     switch (p->mesh->family) {
     case FAM_TRI_P1: return tiled_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return tiled_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);

@@ -37,6 +37,8 @@ __constant__ RefTab<FAM_TRI_P2> c_tab_tri2;
 __constant__ RefTab<FAM_TET_P1> c_tab_tet1;
 __constant__ RefTab<FAM_TET_P2> c_tab_tet2;
 __constant__ RefTab<FAM_TRI_P2_Q16> c_tab_tri2q;
+__constant__ RefTab<FAM_LINE_P1> c_tab_line1;
+__constant__ RefTab<FAM_LINE_P2> c_tab_line2;
 
 template <int F> __device__ __forceinline__ const RefTab<F>& tab();
 template <> __device__ __forceinline__ const RefTab<FAM_TRI_P1>& tab<FAM_TRI_P1>() { return c_tab_tri1; }
@@ -44,6 +46,8 @@ template <> __device__ __forceinline__ const RefTab<FAM_TRI_P2>& tab<FAM_TRI_P2>
 template <> __device__ __forceinline__ const RefTab<FAM_TET_P1>& tab<FAM_TET_P1>() { return c_tab_tet1; }
 template <> __device__ __forceinline__ const RefTab<FAM_TET_P2>& tab<FAM_TET_P2>() { return c_tab_tet2; }
 template <> __device__ __forceinline__ const RefTab<FAM_TRI_P2_Q16>& tab<FAM_TRI_P2_Q16>() { return c_tab_tri2q; }
+template <> __device__ __forceinline__ const RefTab<FAM_LINE_P1>& tab<FAM_LINE_P1>() { return c_tab_line1; }
+template <> __device__ __forceinline__ const RefTab<FAM_LINE_P2>& tab<FAM_LINE_P2>() { return c_tab_line2; }
 
 namespace refhost {
 
@@ -109,6 +113,26 @@ inline Rule rule_tri16() {
     return r;
 }
 
+// Gauss-Legendre on [0, 1] (curves): xi = 1/2 -+ h, weights sum to 1
+inline Rule rule_line(int npts) {
+    Rule r{};
+    r.nq = npts;
+    if (npts == 2) {
+        const double h = 0.5 / std::sqrt(3.0);
+        r.xi[0][0] = 0.5 - h;
+        r.xi[1][0] = 0.5 + h;
+        r.w[0] = r.w[1] = 0.5;
+    } else {
+        const double h = 0.5 * std::sqrt(0.6);
+        r.xi[0][0] = 0.5 - h;
+        r.xi[1][0] = 0.5;
+        r.xi[2][0] = 0.5 + h;
+        r.w[0] = r.w[2] = 5.0 / 18.0;
+        r.w[1] = 4.0 / 9.0;
+    }
+    return r;
+}
+
 inline Rule rule_tet4() {
     Rule r{};
     r.nq = 4;
@@ -162,10 +186,10 @@ inline void basis_eval(int d, int order, const double* xi, double* phi, double (
     }
     static const int e2[3][2] = {{0, 1}, {1, 2}, {2, 0}};
     static const int e3[6][2] = {{0, 1}, {1, 2}, {2, 0}, {0, 3}, {1, 3}, {2, 3}};
-    const int ne = d == 2 ? 3 : 6;
+    const int ne = d == 1 ? 1 : d == 2 ? 3 : 6;
     for (int k = 0; k < ne; ++k) {
-        const int i = d == 2 ? e2[k][0] : e3[k][0];
-        const int j = d == 2 ? e2[k][1] : e3[k][1];
+        const int i = d <= 2 ? e2[k][0] : e3[k][0];
+        const int j = d <= 2 ? e2[k][1] : e3[k][1];
         phi[nv + k] = 4.0 * l[i] * l[j];
         for (int m = 0; m < 3; ++m) dphi[nv + k][m] = 4.0 * (gl[i][m] * l[j] + l[i] * gl[j][m]);
     }

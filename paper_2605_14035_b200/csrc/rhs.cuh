@@ -83,7 +83,11 @@ __device__ __forceinline__ bool rhs_local(int64_t le, const int32_t* __restrict_
         for (int q = 0; q < NQ; ++q) {
             double J[3][D];
             E::jac_at(J0, J1, q, J);
-            if constexpr (D == 2) {
+            if constexpr (D == 1) {
+                const double det = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
+                ok &= (det > 0.0) & (det < INFINITY);
+                wt[q] = T.w[q] * (det * rsqrt_nr(det));
+            } else if constexpr (D == 2) {
                 const double g11 = J[0][0] * J[0][0] + J[1][0] * J[1][0] + J[2][0] * J[2][0];
                 const double g12 = J[0][0] * J[0][1 % D] + J[1][0] * J[1][1 % D] + J[2][0] * J[2][1 % D];
                 const double g22 = J[0][1 % D] * J[0][1 % D] + J[1][1 % D] * J[1][1 % D] + J[2][1 % D] * J[2][1 % D];
@@ -424,12 +428,14 @@ lfem_status run_rhs_tiled(lfem_plan_s* p, const double* coords, const double* u,
 template <int F, int KIND>
 lfem_status run_rhs(lfem_plan_s* p, const double* coords, const double* u, double* out, cudaStream_t s) {
     constexpr int NC = RhsInfo<KIND>::NC, BD = FamInfo<F>::NREF * NC;
-    if (p->variant == LFEM_NUMERIC_TILED) {  // opt-in: measured slower than the two kernels
-        bool ok = false;
-        LFEM_TRY((rhs_prepare_tiled<F, KIND>(p, s, &ok)));
-        if (ok) {
-            p->rhs_last_tiled = 1;
-            return run_rhs_tiled<F, KIND>(p, coords, u, out, s);
+    if constexpr (FamInfo<F>::D >= 2) {  // no tile configuration for curves
+        if (p->variant == LFEM_NUMERIC_TILED) {  // opt-in: measured slower than the two kernels
+            bool ok = false;
+            LFEM_TRY((rhs_prepare_tiled<F, KIND>(p, s, &ok)));
+            if (ok) {
+                p->rhs_last_tiled = 1;
+                return run_rhs_tiled<F, KIND>(p, coords, u, out, s);
+            }
         }
     }
     p->rhs_last_tiled = 0;
@@ -478,6 +484,12 @@ lfem_status rhs_dispatch(lfem_plan_s* p, int kind, const double* coords, const d
     case FAM_TET_P1:
         if (kll) break;
         return run_rhs<FAM_TET_P1, LFEM_RHS_LOAD>(p, coords, u, out, s);
+    case FAM_LINE_P1:
+        if (kll) break;
+        return run_rhs<FAM_LINE_P1, LFEM_RHS_LOAD>(p, coords, u, out, s);
+    case FAM_LINE_P2:
+        if (kll) break;
+        return run_rhs<FAM_LINE_P2, LFEM_RHS_LOAD>(p, coords, u, out, s);
     case FAM_TET_P2:
         if (kll) break;
         return run_rhs<FAM_TET_P2, LFEM_RHS_LOAD>(p, coords, u, out, s);

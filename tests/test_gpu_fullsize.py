@@ -19,7 +19,7 @@ if not torch.cuda.is_available():
 
 from paper_2605_14035_b200 import lfem  # noqa: E402
 
-KINDS = {"C2": ("M", "A"), "C3": ("M", "Aa"), "C4": ("M", "A"), "C5": ("M", "A", "Aa"), "C4P1": ("M", "A")}
+KINDS = {"C2": ("M", "A"), "C3": ("M", "Aa"), "C4": ("M", "A"), "C5": ("M", "A", "Aa"), "C4P1": ("M", "A"), "CURVE2": ("M", "A")}
 
 
 def _run(name, coeff=None):
@@ -115,6 +115,16 @@ def test_C4P1_full():
     _check_sampled(m, kinds, rp, ci, vals, None)
     vol = _properties(m, kinds, plan, vals, None, 3)
     assert abs(vol - 1.0) < 1e-11
+
+
+def test_CURVE2_full():
+    """SURVEY §8(f) N2 curves at scale: P2 unit circle, 2^23 elements; length 2 pi, A 1 = 0."""
+    m, kinds, plan, rp, ci, vals = _run("CURVE2")
+    assert plan.nnz == 8 * m.n_elems  # n vertex rows of 5 entries + n midpoint rows of 3
+    _check_sampled(m, kinds, rp, ci, vals, None)
+    one = torch.ones(m.n_nodes, dtype=torch.float64, device="cuda")
+    assert abs(float(torch.dot(one, _spmv(plan, vals["M"], one))) - 2 * math.pi) < 1e-11
+    assert float(_spmv(plan, vals["A"], one).abs().max()) <= 1e-11 * float(vals["A"].abs().max())
 
 
 def test_C5_full():
