@@ -213,7 +213,8 @@ __global__ void k_copy_rz(const double* __restrict__ src, double* __restrict__ d
 // Workspace of the CG / MCF entry points (plan-owned, lfem_internal.cuh's McfWork).
 static lfem_status mcf_work(lfem_plan_s* p, cudaStream_t s) {
     McfWork& W = p->mcf;
-    if (W.r) return LFEM_OK;
+    if (W.bad) return LFEM_OK;  // allocated last: set only when every buffer exists (a failed call retries)
+    mcf_free(p, s);             // drop the buffers of an earlier partial attempt
     const int64_t n = p->n_rows, nnz = p->nnz;
     for (double** v : {&W.r, &W.z, &W.pv, &W.q, &W.b}) LFEM_TRY(dev_alloc_t(v, (size_t)3 * n + 3, s));
     LFEM_TRY(dev_alloc_t(&W.dinv, (size_t)n + 1, s));
