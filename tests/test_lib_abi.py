@@ -70,3 +70,27 @@ def test_allocator_hook_argument_check_without_gpu(libpath):
     a = ALLOC(lambda n, s, c: None)
     assert lib.lfem_set_allocator(ctypes.cast(a, ctypes.c_void_p), None, None) == 1  # INVALID_ARG
     assert lib.lfem_set_allocator(None, None, None) == 0
+
+
+def header_enums():
+    """NAME = value pairs of the enums in include/lfem.h."""
+    src = open(os.path.join(ROOT, "include", "lfem.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return {k: int(v.rstrip("u")) for k, v in re.findall(r"\b(LFEM_[A-Z0-9_]+)\s*=\s*([0-9]+u?)", src)}
+
+
+def test_binding_constants_match_the_header():
+    """The Python binding's and the input generators' constants are the header's enums."""
+    import lfem_inputs as li
+    from paper_2605_14035_b200 import lfem
+    e = header_enums()
+    for name in ("LFEM_MASS", "LFEM_STIFF", "LFEM_STIFF_COEF", "LFEM_NUMERIC_AUTO", "LFEM_NUMERIC_V0",
+                 "LFEM_NUMERIC_TILED", "LFEM_NUMERIC_ROWS", "LFEM_RHS_LOAD", "LFEM_RHS_KLL"):
+        assert getattr(lfem, name) == e[name], name
+    pairs = {"SURFACE_TRI": "LFEM_SURFACE_TRI", "BULK_TET": "LFEM_BULK_TET", "SURFACE_LINE": "LFEM_SURFACE_LINE",
+             "QUAD_DEFAULT": "LFEM_QUAD_DEFAULT", "QUAD_TRI3_DEG2": "LFEM_QUAD_TRI3_DEG2",
+             "QUAD_TRI6_DEG4": "LFEM_QUAD_TRI6_DEG4", "QUAD_TET4_DEG2": "LFEM_QUAD_TET4_DEG2",
+             "QUAD_TET11_DEG4": "LFEM_QUAD_TET11_DEG4", "QUAD_TRI16_DEG8": "LFEM_QUAD_TRI16_DEG8",
+             "QUAD_LINE2_DEG3": "LFEM_QUAD_LINE2_DEG3", "QUAD_LINE3_DEG5": "LFEM_QUAD_LINE3_DEG5"}
+    for py, h in pairs.items():
+        assert getattr(li, py) == e[h], (py, h)
