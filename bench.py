@@ -66,6 +66,35 @@ def algorithmic_bytes(name, n_elems, nref, n_nodes, nnz, kinds, has_coeff):
     return b
 
 
+# one metric string per workload, shared by the GPU arm and the reference arm (the driver pairs them)
+METRIC_MATRICES = "elements/s (fp64 numeric assembly of all kinds of the config into CSR)"
+
+
+def metric_rhs(kind):
+    return f"elements/s (fp64 {kind} right-hand side assembly)"
+
+
+# configs whose step moves < 4 x L2 (504 MB): L2 flushed (256 MiB write) between timed steps
+FLUSH_L2 = {"C1", "C2", "C3", "C4P1"}
+
+
+def l2_note(name):
+    return "flushed (256 MiB write) between steps" if name in FLUSH_L2 else "inputs+outputs > L2 (126 MB); no flush"
+
+
+def config_matrices(name, m, kinds, world, variant):
+    """The bench line's `config` (identical in the GPU arm and the reference arm)."""
+    return {"workload": f"{name}: {CONFIG_DESC[name]}" + (" [Dunavant-8 rule, 16 points]" if QUAD8 else ""),
+            "kinds": list(kinds), "n_elems": int(m.n_elems), "n_nodes": int(m.n_nodes),
+            "parallelism": f"row-blocks x{world}", "l2": l2_note(name), "variant": variant}
+
+
+def config_rhs(name, m, kind, nc, world, variant):
+    return {"workload": f"{name} mesh ({m.n_elems} elements, {m.n_nodes} nodes), {kind} right-hand "
+                        f"side ({nc} components)" + (", Dunavant-8 rule" if QUAD8 else ""),
+            "rhs": kind, "parallelism": f"row-blocks x{world}", "variant": variant, "l2": l2_note(name)}
+
+
 QUAD8 = False  # --quad8: P2 triangle configs with Dunavant's 16-point degree-8 rule (SURVEY N2, P:727)
 
 
@@ -212,11 +241,11 @@ def run_reference(args):
     t = sum(times)
     equiv = m.n_elems * rows / m.n_nodes * len(times)
     value = equiv / t
-    line = {"impl": "reference", "metric": "elements/s (fp64 numeric assembly, all kinds of the config)",
+    line = {"impl": "reference", "metric": METRIC_MATRICES,
             "value": value, "unit": "elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / len(times), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, lfem_inputs)",
-            "config": {"workload": f"{name}: {CONFIG_DESC[name]}", "kinds": list(kinds)},
+            "config": config_matrices(name, m, kinds, args.gpus, args.variant),
             "cpu_baseline": {"value": value, "unit": "elements/s", "cores": nt, "kind": "oracle",
                              "sample": f"{rows} contiguous rows per step of {m.n_nodes} "
                                        f"(elements/s = n_elems * rows/n_rows / t); per-step sample"},
@@ -246,11 +275,11 @@ def run_reference_rhs(args):
             times.append(time.perf_counter() - t0)
     t = sum(times)
     value = m.n_elems * rows / m.n_nodes * len(times) / t
-    line = {"impl": "reference", "metric": f"elements/s (fp64 {kind} right-hand side assembly)",
+    line = {"impl": "reference", "metric": metric_rhs(kind),
             "value": value, "unit": "elements/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * t / len(times), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded, lfem_inputs)",
-            "config": {"workload": f"{name} mesh, {kind} right-hand side", "rhs": kind},
+            "config": config_rhs(name, m, kind, u.shape[0], args.gpus, args.variant),
             "cpu_baseline": {"value": value, "unit": "elements/s", "cores": nt, "kind": "oracle",
                              "sample": f"{rows} contiguous rows per step of {m.n_nodes}"},
             "e2e": {"value": value, "unit": "elements/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -306,7 +335,7 @@ def run_rhs(args):
         lfem.lfem_assemble_rhs(plan, k, None, u, out)
     lfem.lfem_plan_check(plan)
     alg = rhs_alg_bytes(plan.n_elems_local, m.nref, m.n_nodes, plan.n_rows, nc)
-    flush = alg < 4 * L2_BYTES
+    flush = name in FLUSH_L2
     flush_buf = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
     clocks = ClockSampler(local)
     clocks.start()
@@ -335,6 +364,19 @@ def run_rhs(args):
     prof = lfem.lfem_profile_read(plan)
     lfem.lfem_profile_enable(plan, False)
     clk = clocks.stop()
+    # per-rank shape of the partition (N > 1): rows, nnz, elements assembled (halo included), device ms
+    mine_info = torch.tensor([plan.n_rows, plan.nnz, plan.n_elems_local, elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        parts = [torch.empty_like(mine_info) for _ in range(world)]
+        dist.all_gather(parts, mine_info)
+        info = torch.stack(parts).cpu().numpy()
+    else:
+        info = mine_info.cpu().numpy()[None, :]
+    ranks = {"rows": [int(v) for v in info[:, 0]], "nnz": [int(v) for v in info[:, 1]],
+             "n_elems_local": [int(v) for v in info[:, 2]],
+             "ms_per_step": [float(v) / args.steps for v in info[:, 3]],
+             "nnz_spread_max_over_min": float(info[:, 1].max() / max(1.0, info[:, 1].min())),
+             "halo_factor_per_rank": [float(v) * world / n_elems for v in info[:, 2]]}
     tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -402,15 +444,11 @@ def run_rhs(args):
         cpu = {"value": m.n_elems * rows / m.n_nodes / dt, "unit": "elements/s", "cores": nt, "kind": "oracle",
                "sample": f"rows [0, {rows}) of {m.n_nodes} ({dt:.1f} s); elements/s = n_elems * rows/n_rows / t"}
     if rank == 0:
-        line = {"metric": f"elements/s (fp64 {kind} right-hand side assembly)", "value": value,
+        line = {"metric": metric_rhs(kind), "value": value,
                 "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
                 "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
-                "config": {"workload": f"{name} mesh ({m.n_elems} elements, {m.n_nodes} nodes), {kind} right-hand "
-                                       f"side ({nc} components)" + (", Dunavant-8 rule" if QUAD8 else ""), "rhs": kind, "parallelism": f"row-blocks x{world}",
-                           "variant": args.variant,
-                           "l2": "flushed (256 MiB write) between steps" if flush else
-                                 "inputs+outputs > L2 (126 MB); no flush"},
+                "config": config_rhs(name, m, kind, nc, world, args.variant),
                 "first_call_ms": first_ms, "generate_s": gen_s,
                 "gpu_launches": lfem.lfem_rhs_launches(plan, k) * args.steps,
                 "roofline": roofline, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "verify": verify}
@@ -494,6 +532,19 @@ def run_mcf(args):
     torch.cuda.synchronize()
     prof_step_ms = t0p.elapsed_time(t1p) / nprof
     clk = clocks.stop()
+    # per-rank shape of the partition (N > 1): rows, nnz, elements assembled (halo included), device ms
+    mine_info = torch.tensor([plan.n_rows, plan.nnz, plan.n_elems_local, elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        parts = [torch.empty_like(mine_info) for _ in range(world)]
+        dist.all_gather(parts, mine_info)
+        info = torch.stack(parts).cpu().numpy()
+    else:
+        info = mine_info.cpu().numpy()[None, :]
+    ranks = {"rows": [int(v) for v in info[:, 0]], "nnz": [int(v) for v in info[:, 1]],
+             "n_elems_local": [int(v) for v in info[:, 2]],
+             "ms_per_step": [float(v) / args.steps for v in info[:, 3]],
+             "nnz_spread_max_over_min": float(info[:, 1].max() / max(1.0, info[:, 1].min())),
+             "halo_factor_per_rank": [float(v) * world / n_elems for v in info[:, 2]]}
     tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -659,9 +710,13 @@ def run_lfem(args):
     dev = torch.device("cuda", local)
     if world > 1:
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # communicator init (ranks, NVLink / NVLS paths) in the log
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        log(f"rank {rank}/{world}: {backend} process group on cuda:{local}"
+            + (f", NCCL {torch.cuda.nccl.version()}" if backend == "nccl" else ""))
     name = args.config
 
     # ---- inputs: rank 0 generates (seeded), broadcast over NCCL (plumbing, untimed)
@@ -736,7 +791,7 @@ def run_lfem(args):
     nnz_total, elems_local_total = int(tot[0]), int(tot[1])
     alg_bytes_rank = algorithmic_bytes(name, plan.n_elems_local, nref, plan.n_rows, plan.nnz, kinds, has_coeff)
     alg_bytes_total = algorithmic_bytes(name, n_elems, nref, n_nodes, nnz_total, kinds, has_coeff)
-    flush = alg_bytes_rank < 4 * L2_BYTES
+    flush = name in FLUSH_L2
     flush_buf = torch.empty(256 * 2 ** 20 // 4, dtype=torch.float32, device=dev) if flush else None
 
     # first call builds the TILED variant's tile plan (one-time, like the symbolic phase): timed apart
@@ -787,7 +842,21 @@ def run_lfem(args):
     prof = lfem.lfem_profile_read(plan)
     lfem.lfem_profile_enable(plan, False)
     clk = clocks.stop()
+    evals, n_tiles = lfem.lfem_numeric_stats(plan)
 
+    # per-rank shape of the partition (N > 1): rows, nnz, elements assembled (halo included), device ms
+    mine_info = torch.tensor([plan.n_rows, plan.nnz, plan.n_elems_local, elapsed_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        parts = [torch.empty_like(mine_info) for _ in range(world)]
+        dist.all_gather(parts, mine_info)
+        info = torch.stack(parts).cpu().numpy()
+    else:
+        info = mine_info.cpu().numpy()[None, :]
+    ranks = {"rows": [int(v) for v in info[:, 0]], "nnz": [int(v) for v in info[:, 1]],
+             "n_elems_local": [int(v) for v in info[:, 2]],
+             "ms_per_step": [float(v) / args.steps for v in info[:, 3]],
+             "nnz_spread_max_over_min": float(info[:, 1].max() / max(1.0, info[:, 1].min())),
+             "halo_factor_per_rank": [float(v) * world / n_elems for v in info[:, 2]]}
     tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -900,23 +969,22 @@ def run_lfem(args):
 
     if rank == 0:
         line = {
-            "metric": "elements/s (fp64 numeric assembly of all kinds of the config into CSR)",
+            "metric": METRIC_MATRICES,
             "value": value, "unit": "elements/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic (seeded generators, lfem_inputs)",
-            "config": {"workload": f"{name}: {CONFIG_DESC[name]}" + (" [Dunavant-8 rule, 16 points]" if QUAD8 else ""),
-                       "kinds": list(kinds), "n_elems": n_elems,
-                       "n_nodes": n_nodes, "nnz": nnz_total, "parallelism": f"row-blocks x{world}",
-                       "l2": "flushed (256 MiB write) between steps" if flush else
-                             "inputs+outputs > L2 (126 MB); no flush", "variant": args.variant},
+            "config": config_matrices(name, m, kinds, world, args.variant), "nnz": nnz_total,
             "nnz_per_s": nnz_total * args.steps / (elapsed_ms * 1e-3),
             "value_slots_per_s": len(kinds) * nnz_total * args.steps / (elapsed_ms * 1e-3),
             "symbolic_ms": symbolic_ms, "first_numeric_call_ms": first_call_ms, "generate_s": gen_s,
-            "halo_factor": elems_local_total / n_elems,
+            "halo_factor": elems_local_total / n_elems, "ranks": ranks if world > 1 else None,
             "gpu_launches": (lfem.lfem_numeric_launches(plan, kmask) + (1 if u_work is not None else 0)) * args.steps,
             "roofline": roofline,
             "fp64": {"flop_model_per_elem": FLOP_PER_ELEM[name],
-                     "achieved_tflops": FLOP_PER_ELEM[name] * plan.n_elems_local / (step_kernel_ms * 1e-3) / 1e12},
+                     "achieved_tflops": FLOP_PER_ELEM[name] * plan.n_elems_local / (step_kernel_ms * 1e-3) / 1e12,
+                     # element evaluations the kernel actually performs (tile halo recompute included)
+                     "elem_evals_per_step": evals, "processed_factor": evals / max(1, plan.n_elems_local),
+                     "executed_tflops": FLOP_PER_ELEM[name] * evals / (step_kernel_ms * 1e-3) / 1e12},
             "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "verify": verify,
         }
         print(json.dumps(line), flush=True)

@@ -47,11 +47,22 @@
  *    of the numeric variant's tiling and of the row-block partition (each CSR
  *    slot sums its contributions in ascending element id, then local (a,b);
  *    reading G21).  No floating-point atomics anywhere.
- *  - Limits: n_nodes, n_elems < 2^31; local entries n_elems_local*nref^2 < 2^31;
- *    per row at most 512 candidate (element, column) entries (a P2 tet vertex
- *    shared by <= 51 tets); TILED: a row may touch at most the tile capacity
- *    of elements (256 P2 / 1024 P1 triangles, 128 P2 / 256 P1 tets) and a CSR
- *    slot at most 254 contributions; violations return LFEM_ERR_UNSUPPORTED.
+ *  - Limits: n_nodes, n_elems < 2^31; local entries n_elems_local*nref^2 < 2^31.
+ *    Rows with more than 512 candidate (element, column) entries (e.g. a P2 tet
+ *    vertex shared by more than 51 tets) take a slower one-CTA-per-row path of
+ *    the symbolic phase (at most 65536 such rows).  TILED: a row may touch at
+ *    most the tile capacity of elements (256 P2 / 1024 P1 triangles, 128 P2 /
+ *    256 P1 tets) and a CSR slot at most 254 contributions; an explicit TILED
+ *    request then returns LFEM_ERR_UNSUPPORTED, AUTO runs V0 on that plan.
+ *  - Alignment: double arrays (coords, coeff, vals, u, out) 8-byte aligned and
+ *    int32 arrays 4-byte aligned, else LFEM_ERR_INVALID_ARG.  The TILED kernel
+ *    copies coords and coeff with cp.async.bulk (16-byte aligned sources) and
+ *    writes vals with 16-byte stores: if any of them is only 8-byte aligned,
+ *    AUTO runs V0 and an explicit TILED request returns LFEM_ERR_INVALID_ARG
+ *    (no misaligned-address fault).
+ *  - Device allocations of plans (and of lfem_mesh_create's index check) are
+ *    stream-ordered on the call's stream (cudaMallocAsync / cudaFreeAsync)
+ *    unless a hook is installed (lfem_set_allocator).
  */
 #ifndef LFEM_H_
 #define LFEM_H_
@@ -140,6 +151,8 @@ void lfem_mesh_destroy(lfem_mesh m);
  * The mesh must outlive the plan. */
 lfem_status lfem_assemble_symbolic(lfem_mesh m, int64_t row_begin, int64_t row_end,
                                    lfem_stream_t stream, lfem_plan* out);
+/* Waits for the work this plan enqueued (an event per stream it ran on; not a
+ * device-wide sync), then frees the plan. */
 void lfem_plan_destroy(lfem_plan p);
 
 /* n_rows = row_end - row_begin; nnz of the block; n_elems_local = elements touching it. */
@@ -255,7 +268,10 @@ lfem_status lfem_spmv(lfem_plan p, const double* vals, const double* x_full, dou
                       lfem_stream_t stream);
 
 /* Synchronises `stream`, then reports latched device errors
- * (LFEM_ERR_DEGENERATE with the lowest element id). */
+ * (LFEM_ERR_DEGENERATE with the lowest element id).  A reported error is
+ * cleared: the latch holds the lowest bad element of the calls enqueued since
+ * the last check (lfem_assemble_numeric_host checks at its end), so a plan
+ * reused with valid coordinates after a degenerate call reports OK again. */
 lfem_status lfem_plan_check(lfem_plan p, lfem_stream_t stream);
 
 /* out[i] = ca * a[i] + cb * b[i], i < n (device; the C3 coefficient update
@@ -274,14 +290,20 @@ lfem_status lfem_profile_read(lfem_plan p, int max, const char** names, double* 
 /* Number of kernel launches lfem_assemble_numeric enqueues for this plan and kinds. */
 int lfem_numeric_launches(lfem_plan p, unsigned kinds);
 
+/* Work of the last numeric call on this plan: elem_evals = element evaluations
+ * (geometry + local matrices) per call -- n_elems_local for V0 / ROWS, the sum
+ * of the tiles' element lists (halo elements counted once per tile) for TILED;
+ * n_tiles = row tiles of the TILED plan (0 otherwise).  Either pointer may be NULL. */
+lfem_status lfem_numeric_stats(lfem_plan p, int64_t* elem_evals, int64_t* n_tiles);
+
 /* Device-memory allocator hook (a user's caching allocator,
  * e.g. PyTorch's).  Every device allocation of meshes and plans (plan arrays,
  * tile plan, V0 stage, e2e staging) goes through alloc(bytes, stream, ctx)
  * and is released with dealloc(ptr, stream, ctx) on the stream it was used on;
  * alloc returns a 256-B aligned device pointer or NULL (-> LFEM_ERR_NOMEM).
- * NULL, NULL restores cudaMalloc / cudaFree.  Process-wide; may be changed at
+ * NULL, NULL restores cudaMallocAsync / cudaFreeAsync on the call's stream.  Process-wide; may be changed at
  * any time: every pointer is released by the allocator (hook + ctx, or
- * cudaFree) that produced it.  INVALID_ARG if exactly one of alloc / dealloc
+ * cudaFreeAsync) that produced it.  INVALID_ARG if exactly one of alloc / dealloc
  * is NULL. */
 typedef void* (*lfem_alloc_fn)(size_t bytes, lfem_stream_t stream, void* ctx);
 typedef void (*lfem_free_fn)(void* ptr, lfem_stream_t stream, void* ctx);

@@ -427,20 +427,28 @@ int element_rhs(const Ref& R, const double* X, const double* U, int kind, int fo
         double weight = w * mu;
         double wabs = std::fabs(w) * mu;
         if (kind == RHS_KLL) {
-            double alpha2 = 0.0, alpha2_abs = 0.0;
+            // grad_Gamma_h nu_k = sum_c nu_ck g_c = sum_{c>=2} (nu_ck - nu_1k) g_c, since
+            // sum_c g_c = J G^-1 sum_c grad phi_c = 0 (differences as for J, reading G24).
+            // Tolerance scale (reading G33): the first-order rounding error of
+            // alpha^2 = sum_k |G_k|^2 is 2 sum_k |G_k| |dG_k| with |dG_k| <~ eps B_k,
+            // B_k = sum_{c>=2} |nu_ck - nu_1k| |g_c|, so alpha^2 is scaled by
+            // alpha^2 + 2 sum_k |G_k| B_k.
+            double alpha2 = 0.0, cross = 0.0;
             for (int k = 0; k < 3; ++k) {
                 double grad_nu_k[3] = {0.0, 0.0, 0.0};  // grad_Gamma_h of component k of nu_h
-                double bound_k = 0.0;                   // sum_c |nu_ck| |g_c|
-                for (int c = 0; c < n; ++c) {
-                    for (int i = 0; i < 3; ++i) grad_nu_k[i] += U[c * nc + k] * g[c][i];
-                    bound_k += std::fabs(U[c * nc + k]) *
-                               std::sqrt(g[c][0] * g[c][0] + g[c][1] * g[c][1] + g[c][2] * g[c][2]);
+                double bound_k = 0.0;                   // B_k
+                for (int c = 1; c < n; ++c) {
+                    const double d = U[c * nc + k] - U[k];
+                    for (int i = 0; i < 3; ++i) grad_nu_k[i] += d * g[c][i];
+                    bound_k += std::fabs(d) * std::sqrt(g[c][0] * g[c][0] + g[c][1] * g[c][1] + g[c][2] * g[c][2]);
                 }
-                for (int i = 0; i < 3; ++i) alpha2 += grad_nu_k[i] * grad_nu_k[i];
-                alpha2_abs += bound_k * bound_k;
+                double gk2 = 0.0;
+                for (int i = 0; i < 3; ++i) gk2 += grad_nu_k[i] * grad_nu_k[i];
+                alpha2 += gk2;
+                cross += std::sqrt(gk2) * bound_k;
             }
             weight *= alpha2;
-            wabs *= alpha2_abs;
+            wabs *= alpha2 + 2.0 * cross;
         }
         for (int a = 0; a < n; ++a)
             for (int k = 0; k < nc; ++k) F[a * nc + k] += weight * uq[k] * R.phi[q][a];

@@ -1,5 +1,6 @@
 // C ABI of liblfem (include/lfem.h): handles, argument checking, errors.
 #include <climits>
+#include <map>
 #include <mutex>
 #include <unordered_map>
 #include <cstdio>
@@ -74,6 +75,8 @@ thread_local int64_t g_err_elem = -1;
 cudaStream_t S(lfem_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
 
 void free_plan_memory(lfem_plan_s* p) {
+    // every stream that ran work on the plan is done (lfem_plan_destroy waited on the
+    // plan's events), so the frees may be ordered on the legacy stream
     cudaStream_t s = nullptr;
     dev_free(p->elem_list, s);
     dev_free(p->local_conn, s);
@@ -139,11 +142,12 @@ lfem_status dev_alloc(void** p, size_t bytes, cudaStream_t s) {
         g_hooked[*p] = h;
         return LFEM_OK;
     }
-    cudaError_t e = cudaMalloc(p, bytes);
+    // default: stream-ordered allocation on the call's stream (SURVEY.md §8(b) conventions)
+    cudaError_t e = cudaMallocAsync(p, bytes, s);
     if (e != cudaSuccess) {
         cudaGetLastError();
         *p = nullptr;
-        return lfem_fail(LFEM_ERR_NOMEM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed");
+        return lfem_fail(LFEM_ERR_NOMEM, "cudaMallocAsync of " + std::to_string(bytes) + " bytes failed");
     }
     return LFEM_OK;
 }
@@ -163,7 +167,43 @@ void dev_free(void* p, cudaStream_t s) {
         h.dealloc(p, reinterpret_cast<lfem_stream_t>(s), h.ctx);
         return;
     }
-    cudaFree(p);
+    cudaFreeAsync(p, s);
+}
+
+namespace {
+std::mutex g_attr_mu;
+std::map<std::pair<int, const void*>, int> g_attr;  // (device, kernel) -> opted-in dynamic smem bytes
+}  // namespace
+
+lfem_status ensure_smem_attr(const void* func, int bytes) {
+    int dev = 0;
+    LFEM_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    int& have = g_attr[{dev, func}];
+    if (have >= bytes) return LFEM_OK;
+    LFEM_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    have = bytes;
+    return LFEM_OK;
+}
+
+lfem_status device_sm_count(int* sms) {
+    int dev = 0;
+    LFEM_CUDA(cudaGetDevice(&dev));
+    LFEM_CUDA(cudaDeviceGetAttribute(sms, cudaDevAttrMultiProcessorCount, dev));
+    return LFEM_OK;
+}
+
+lfem_status plan_mark(lfem_plan_s* p, cudaStream_t s) {
+    for (auto& d : p->done)
+        if (d.first == s) {
+            LFEM_CUDA(cudaEventRecord(d.second, s));
+            return LFEM_OK;
+        }
+    cudaEvent_t ev = nullptr;
+    LFEM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    p->done.push_back({s, ev});
+    LFEM_CUDA(cudaEventRecord(ev, s));
+    return LFEM_OK;
 }
 
 extern "C" {
@@ -207,6 +247,8 @@ lfem_status lfem_mesh_create(lfem_domain dom, int order, lfem_quad quad, int64_t
         return lfem_fail(LFEM_ERR_INVALID_ARG, "n_nodes / n_elems out of range");
     if ((n_nodes > 0 && !coords) || (n_elems > 0 && !conn))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "coords / conn is NULL");
+    if ((reinterpret_cast<uintptr_t>(coords) & 7) || (reinterpret_cast<uintptr_t>(conn) & 3))
+        return lfem_fail(LFEM_ERR_INVALID_ARG, "coords must be 8-byte and conn 4-byte aligned");
     static const int nrefs[7] = {3, 6, 4, 10, 6, 2, 3};
     static const int nqs[7] = {3, 6, 4, 11, 16, 2, 3};
     static const int nsyms[7] = {6, 21, 10, 55, 21, 3, 6};
@@ -273,8 +315,11 @@ lfem_status lfem_assemble_symbolic(lfem_mesh m, int64_t row_begin, int64_t row_e
         if (e != cudaSuccess) st = lfem_cuda_fail(e, "cudaMemcpyAsync");
     }
     if (st == LFEM_OK) st = build_symbolic(p, S(stream));
+    if (st == LFEM_OK) st = plan_mark(p, S(stream));
     if (st != LFEM_OK) {
+        cudaStreamSynchronize(S(stream));
         free_plan_memory(p);
+        cudaStreamSynchronize(nullptr);
         delete p;
         return st;
     }
@@ -284,8 +329,14 @@ lfem_status lfem_assemble_symbolic(lfem_mesh m, int64_t row_begin, int64_t row_e
 
 void lfem_plan_destroy(lfem_plan p) {
     if (!p) return;
-    cudaDeviceSynchronize();
+    // wait for the work enqueued on this plan (one event per stream it ran on), not the device
+    for (auto& d : p->done) {
+        cudaEventSynchronize(d.second);
+        cudaEventDestroy(d.second);
+    }
+    p->done.clear();
     free_plan_memory(p);
+    cudaStreamSynchronize(nullptr);  // the frees above were ordered on the legacy stream
     delete p;
 }
 
@@ -302,11 +353,19 @@ lfem_status lfem_plan_set_variant(lfem_plan p, lfem_numeric_variant v) {
     if (v != LFEM_NUMERIC_AUTO && v != LFEM_NUMERIC_V0 && v != LFEM_NUMERIC_TILED && v != LFEM_NUMERIC_ROWS)
         return lfem_fail(LFEM_ERR_INVALID_ARG, "variant");
     p->variant = v;
+    p->last_variant = -1;
     return LFEM_OK;
 }
 
+static bool misaligned(const void* q, uintptr_t a) { return (reinterpret_cast<uintptr_t>(q) & (a - 1)) != 0; }
+
 static lfem_status check_numeric_args(lfem_plan p, unsigned kinds, const double* coeff, double* const vals[3]) {
     if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
+    if (misaligned(coeff, 8)) return lfem_fail(LFEM_ERR_INVALID_ARG, "coeff is not 8-byte aligned");
+    if (vals)
+        for (int k = 0; k < 3; ++k)
+            if (((kinds >> k) & 1u) && misaligned(vals[k], 8))
+                return lfem_fail(LFEM_ERR_INVALID_ARG, "vals[k] is not 8-byte aligned");
     if (kinds == 0 || (kinds & ~7u))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "kinds must be a nonzero subset of MASS|STIFF|STIFF_COEF");
     if ((kinds & LFEM_STIFF_COEF) && !coeff && p->mesh->n_nodes > 0)
@@ -327,7 +386,8 @@ lfem_status lfem_assemble_numeric(lfem_plan p, unsigned kinds, const double* coe
     LFEM_TRY(check_numeric_args(p, kinds, coeff, vals));
     double* v[3];
     for (int k = 0; k < 3; ++k) v[k] = ((kinds >> k) & 1u) ? vals[k] : nullptr;
-    return numeric_dispatch(p, kinds, p->mesh->coords, coeff, v, S(stream));
+    LFEM_TRY(numeric_dispatch(p, kinds, p->mesh->coords, coeff, v, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 lfem_status lfem_assemble_numeric_coords(lfem_plan p, unsigned kinds, const double* coords, const double* coeff,
@@ -336,9 +396,11 @@ lfem_status lfem_assemble_numeric_coords(lfem_plan p, unsigned kinds, const doub
     g_err_elem = -1;
     LFEM_TRY(check_numeric_args(p, kinds, coeff, vals));
     if (!coords && p->mesh->n_nodes > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "coords is NULL");
+    if (misaligned(coords, 8)) return lfem_fail(LFEM_ERR_INVALID_ARG, "coords is not 8-byte aligned");
     double* v[3];
     for (int k = 0; k < 3; ++k) v[k] = ((kinds >> k) & 1u) ? vals[k] : nullptr;
-    return numeric_dispatch(p, kinds, coords, coeff, v, S(stream));
+    LFEM_TRY(numeric_dispatch(p, kinds, coords, coeff, v, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 lfem_status lfem_assemble_numeric_host(lfem_plan p, unsigned kinds, const double* coords_h, const double* coeff_h,
@@ -367,6 +429,7 @@ lfem_status lfem_assemble_numeric_host(lfem_plan p, unsigned kinds, const double
             v[k] = p->d_vals[k];
         }
     LFEM_TRY(numeric_dispatch(p, kinds, coords, coeff, v, s));
+    LFEM_TRY(plan_mark(p, s));
     for (int k = 0; k < 3; ++k)
         if (((kinds >> k) & 1u) && p->nnz > 0)
             LFEM_CUDA(cudaMemcpyAsync(vals_h[k], v[k], sizeof(double) * p->nnz, cudaMemcpyDeviceToHost, s));
@@ -384,7 +447,8 @@ lfem_status lfem_spmv(lfem_plan p, const double* vals, const double* x_full, dou
     if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
     if ((p->nnz > 0 && !vals) || (p->n_rows > 0 && (!x_full || !y_rows)))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL vector");
-    return spmv_launch(p, vals, x_full, y_rows, S(stream));
+    LFEM_TRY(spmv_launch(p, vals, x_full, y_rows, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 int lfem_rhs_ncomp(int kind) { return kind == LFEM_RHS_LOAD ? 1 : kind == LFEM_RHS_KLL ? 4 : 0; }
@@ -404,7 +468,10 @@ lfem_status lfem_assemble_rhs(lfem_plan p, int kind, const double* coords, const
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "the KLL right-hand side is defined on surfaces only");
     if (!u && p->mesh->n_nodes > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "u is NULL");
     if (!out && p->n_rows > 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "out is NULL");
-    return rhs_dispatch(p, kind, coords ? coords : p->mesh->coords, u, out, S(stream));
+    if (misaligned(coords, 8) || misaligned(u, 8) || misaligned(out, 8))
+        return lfem_fail(LFEM_ERR_INVALID_ARG, "coords / u / out is not 8-byte aligned");
+    LFEM_TRY(rhs_dispatch(p, kind, coords ? coords : p->mesh->coords, u, out, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, double* x, double tol, int max_it,
@@ -414,7 +481,8 @@ lfem_status lfem_cg_solve(lfem_plan p, const double* vals_K, const double* b, do
     if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
     if (p->n_rows > 0 && (!vals_K || !b || !x)) return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL argument");
     if (!(tol > 0.0) || max_it < 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "tol must be > 0 and max_it >= 0");
-    return cg_solve(p, vals_K, b, x, tol, max_it, iters, S(stream));
+    LFEM_TRY(cg_solve(p, vals_K, b, x, tol, max_it, iters, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 lfem_status lfem_solve_meanfree(lfem_plan p, const double* vals_A, const double* b, double* u, double tol,
@@ -424,7 +492,8 @@ lfem_status lfem_solve_meanfree(lfem_plan p, const double* vals_A, const double*
     if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
     if (p->n_rows > 0 && (!vals_A || !b || !u)) return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL argument");
     if (!(tol > 0.0) || max_it < 0) return lfem_fail(LFEM_ERR_INVALID_ARG, "tol must be > 0 and max_it >= 0");
-    return solve_meanfree(p, vals_A, b, u, tol, max_it, iters, S(stream));
+    LFEM_TRY(solve_meanfree(p, vals_A, b, u, tol, max_it, iters, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 lfem_status lfem_mcf_step(lfem_plan p, double tau, const double* x_prev, double* x_next, double tol, int max_it,
@@ -437,7 +506,8 @@ lfem_status lfem_mcf_step(lfem_plan p, double tau, const double* x_prev, double*
     if (p->n_rows > 0 && (!x_prev || !x_next)) return lfem_fail(LFEM_ERR_INVALID_ARG, "NULL argument");
     if (!(tau > 0.0) || !(tol > 0.0) || max_it < 0)
         return lfem_fail(LFEM_ERR_INVALID_ARG, "tau and tol must be > 0, max_it >= 0");
-    return mcf_step(p, tau, x_prev, x_next, tol, max_it, iters, S(stream));
+    LFEM_TRY(mcf_step(p, tau, x_prev, x_next, tol, max_it, iters, S(stream)));
+    return plan_mark(p, S(stream));
 }
 
 lfem_status lfem_plan_check(lfem_plan p, lfem_stream_t stream) {
@@ -445,8 +515,13 @@ lfem_status lfem_plan_check(lfem_plan p, lfem_stream_t stream) {
     int h = INT_MAX;
     LFEM_CUDA(cudaStreamSynchronize(S(stream)));
     LFEM_CUDA(cudaMemcpy(&h, p->err, sizeof(int), cudaMemcpyDeviceToHost));
-    if (h != INT_MAX)
+    if (h != INT_MAX) {
+        // surfaced once: clear the latch so later calls on the plan (e.g. valid moving
+        // coordinates) report their own state
+        const int init = INT_MAX;
+        LFEM_CUDA(cudaMemcpy(p->err, &init, sizeof(int), cudaMemcpyHostToDevice));
         return lfem_fail(LFEM_ERR_DEGENERATE, "degenerate element (mu <= 0 or non-finite at a quadrature point)", h);
+    }
     return LFEM_OK;
 }
 
@@ -479,6 +554,14 @@ lfem_status lfem_profile_read(lfem_plan p, int max, const char** names, double* 
         P.count[i] = 0;
     }
     *n = k;
+    return LFEM_OK;
+}
+
+lfem_status lfem_numeric_stats(lfem_plan p, int64_t* elem_evals, int64_t* n_tiles) {
+    if (!p) return lfem_fail(LFEM_ERR_INVALID_ARG, "plan is NULL");
+    const bool tiled = p->last_variant == LFEM_NUMERIC_TILED && p->tiled_ok == 1;
+    if (elem_evals) *elem_evals = tiled ? p->tiles.total_elems : p->n_local;
+    if (n_tiles) *n_tiles = tiled ? p->tiles.n_tiles : 0;
     return LFEM_OK;
 }
 

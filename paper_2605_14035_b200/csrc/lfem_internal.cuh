@@ -4,6 +4,7 @@
 #include <stdint.h>
 
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/lfem.h"
@@ -51,6 +52,7 @@ struct TilePlan {
     int heavy_words = 8;        // u16 words per heavy entry (16-B multiple)
     int32_t* tile_elems = nullptr;      // plan-local element ids, ascending per tile
     int max_tile_nodes = 0;     // max owned rows + halo nodes per tile
+    int64_t total_elems = 0;    // element evaluations per numeric call (tile halo included)
     uint16_t* conn16 = nullptr;         // per tile: its elements' tile-local node indices (16-B padded)
     int32_t* halo = nullptr;            // per tile: halo nodes (global ids, sorted; 16-B padded)
     int4* tile_info = nullptr;          // 3 per tile: {s0, ns, e0, ne}, {q0, nq, h0, nh}, {g0, nrows, l0, nl}
@@ -97,7 +99,14 @@ struct lfem_plan_s {
     int rhs_last_tiled = -1;        // variant of the last lfem_assemble_rhs call (1 fused, 0 two-kernel)
     McfWork mcf;                    // CG / MCF workspace (mcf.cu)
     int rows_ok = -1;               // ROWS variant (rows.cuh): -1 unknown, 1 every row fits, 0 fall back to V0
+    int tiled_ok = -1;              // TILED tile plan: -1 not built, 1 built, 0 unsupported (AUTO runs V0)
+    int last_variant = -1;          // variant the last numeric call ran (after AUTO / alignment fallbacks)
+    // completion events of the calls that enqueued work on this plan, one per stream
+    // (lfem_plan_destroy waits for them instead of the whole device)
+    std::vector<std::pair<cudaStream_t, cudaEvent_t>> done;
 };
+// record that plan p has work enqueued on stream s (lfem_plan_destroy waits for it)
+lfem_status plan_mark(lfem_plan_s* p, cudaStream_t s);
 
 // ---------------------------------------------------------------------------
 // error state (thread-local, set by every failing entry point)
@@ -117,7 +126,12 @@ lfem_status lfem_cuda_fail(cudaError_t e, const char* what);
         if (s_ != LFEM_OK) return s_;                              \
     } while (0)
 
-// device memory helpers (cudaMallocAsync on the plan's stream)
+// Per-(device, kernel) launch attribute cache: one process may drive several
+// devices, so nothing launch-related is cached per process.
+lfem_status ensure_smem_attr(const void* func, int bytes);
+lfem_status device_sm_count(int* sms);
+
+// device memory helpers (cudaMallocAsync on the given stream, or the caller's hook)
 lfem_status dev_alloc(void** p, size_t bytes, cudaStream_t s);
 void dev_free(void* p, cudaStream_t s);
 template <class T>

@@ -182,12 +182,7 @@ lfem_status run_v0(lfem_plan_s* p, const double* coords, const double* coeff, do
         prof_begin(p, "k_elem_v0", s);
         constexpr int BD = v0_block_doubles<F, DM, DA, DAA>();
         constexpr size_t smem = sizeof(double) * (size_t)V0_THREADS * BD;
-        static bool attr = false;  // per instantiation
-        if (!attr) {
-            LFEM_CUDA(cudaFuncSetAttribute(k_elem_v0<F, DM, DA, DAA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-            attr = true;
-        }
+        LFEM_TRY(ensure_smem_attr(reinterpret_cast<const void*>(k_elem_v0<F, DM, DA, DAA>), (int)smem));
         k_elem_v0<F, DM, DA, DAA><<<grid_for(p->n_local, V0_THREADS, 1 << 20), V0_THREADS, smem, s>>>(
             p->n_local, p->local_conn, p->elem_list, coords, coeff, p->stage, p->err);
         LFEM_CUDA(cudaGetLastError());
@@ -317,13 +312,36 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
                              double* const vals[3], cudaStream_t s) {
     LFEM_TRY(upload_reference_tables());
     const int fam = p->mesh->family;
-    const int variant = p->variant == LFEM_NUMERIC_AUTO ? auto_variant(p) : p->variant;
-    if (variant == LFEM_NUMERIC_TILED) return tiled_dispatch(p, kinds, coords, coeff, vals, s);
+    const bool autov = p->variant == LFEM_NUMERIC_AUTO;
+    int variant = autov ? auto_variant(p) : p->variant;
+    if (variant == LFEM_NUMERIC_TILED) {
+        // the tile kernel moves coords / coeff with cp.async.bulk (16-byte aligned sources) and
+        // stores value pairs with 16-byte vector stores
+        uintptr_t al = reinterpret_cast<uintptr_t>(coords) | reinterpret_cast<uintptr_t>(coeff);
+        for (int k = 0; k < 3; ++k) al |= reinterpret_cast<uintptr_t>(vals[k]);
+        const bool aligned = (al & 15) == 0;
+        if (!aligned && !autov)
+            return lfem_fail(LFEM_ERR_INVALID_ARG, "the TILED variant needs 16-byte aligned coords, coeff and vals");
+        if (aligned && !(autov && p->tiled_ok == 0)) {
+            const lfem_status st = tiled_dispatch(p, kinds, coords, coeff, vals, s);
+            if (st == LFEM_OK) {
+                p->last_variant = LFEM_NUMERIC_TILED;
+                return LFEM_OK;
+            }
+            // AUTO: a mesh the tile plan cannot hold (e.g. a very high-valence row) runs V0
+            if (!(autov && st == LFEM_ERR_UNSUPPORTED && p->tiled_ok == 0)) return st;
+        }
+        variant = LFEM_NUMERIC_V0;
+    }
     if (variant == LFEM_NUMERIC_ROWS) {
         bool ok = false;
         LFEM_TRY(rows_dispatch(p, kinds, coords, coeff, vals, s, &ok));
-        if (ok) return LFEM_OK;  // else: a row longer than the ROWS lanes hold -> V0
+        if (ok) {
+            p->last_variant = LFEM_NUMERIC_ROWS;
+            return LFEM_OK;  // else: a row longer than the ROWS lanes hold -> V0
+        }
     }
+    p->last_variant = LFEM_NUMERIC_V0;
     switch (fam) {
     case FAM_TRI_P1: return dispatch_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return dispatch_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);
@@ -338,7 +356,8 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
 
 int numeric_launch_count(lfem_plan_s* p, unsigned kinds) {
     (void)kinds;
-    const int variant = p->variant == LFEM_NUMERIC_AUTO ? auto_variant(p) : p->variant;
+    int variant = p->last_variant >= 0 ? p->last_variant
+                                       : p->variant == LFEM_NUMERIC_AUTO ? auto_variant(p) : p->variant;
     if (variant == LFEM_NUMERIC_TILED) return tiled_launch_count(p);
     if (variant == LFEM_NUMERIC_ROWS && p->rows_ok != 0) return p->n_rows > 0 ? 1 : 0;
     return (p->n_local > 0 ? 1 : 0) + (p->nnz > 0 ? 1 : 0);

@@ -34,8 +34,7 @@
 #ifndef LFEM_P1_EPT
 #define LFEM_P1_EPT 4
 #endif
-#ifndef LFEM_P1_RU  // P1 triangles (C3): measured best with 2 chunks per reduce iteration, 176/80 registers
-#define LFEM_P1_RU 2
+#ifndef LFEM_P1_REGS_C  // P1 triangles (C3): register split measured best in round 1
 #define LFEM_P1_REGS_C 176
 #define LFEM_P1_REGS_R 80
 #endif
@@ -61,9 +60,7 @@
 #ifndef LFEM_NSB  // stage buffers (kind passes in flight between compute and reduce warps)
 #define LFEM_NSB 2
 #endif
-#ifndef LFEM_RU
-#define LFEM_RU 3  // light chunks per reduce iteration (P2): measured 3 > 4 > 2 > 5, 8 on C5
-#endif
+
 
 namespace {
 
@@ -109,29 +106,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     } while (!done);
 }
 
-// per-role phase accounting (debug bit 2; timing experiments only)
-struct PhaseClock {
-    bool on;
-    long long t0;
-    __device__ __forceinline__ void start() { if (on) t0 = clock64(); }
-    __device__ __forceinline__ void lap(unsigned long long* acc, int k) {
-        if (on) { const long long t = clock64(); atomicAdd(&acc[k], (unsigned long long)(t - t0)); t0 = t; }
-    }
-};
+// timing experiments only (compile-time, scripts/build_variants.py -DLFEM_TILED_SKIP=..):
+// bit0 compute warps skip the kind contractions, bit1 reduce warps skip the slots
+#ifndef LFEM_TILED_SKIP
+#define LFEM_TILED_SKIP 0
+#endif
 
 __device__ __forceinline__ void st_stream(double* p, double v) {
     asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
 }
 
 // CW compute warps, RW reduce warps, EPT elements per compute thread (tile
-// element budget CW*32*EPT), RU light-slot chunks per reduce iteration,
-// REGS_C / REGS_R setmaxnreg budgets of the two roles (0 = launch default).
+// element budget CW*32*EPT), REGS_C / REGS_R setmaxnreg budgets of the two
+// roles (0 = launch default).
 template <int F> struct TileCfg;
-template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, RU = LFEM_P1_RU, MINB = 1, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
-template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = LFEM_P2_EPT, RU = LFEM_RU, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
+template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, MINB = 1, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
+template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = LFEM_P2_EPT, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
 template <> struct TileCfg<FAM_TRI_P2_Q16> : TileCfg<FAM_TRI_P2> {};
-template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
-template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, MINB = 1, EPT = 1, RU = 2, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, MINB = 1, EPT = 1, REGS_C = 0, REGS_R = 0; };
 
 struct TileLayout {
     size_t stage_bytes;           // one stage buffer
@@ -176,9 +169,6 @@ struct TileArgs {
     const double* coeff;
     double* v[3];
     int* err;
-    int debug;  // timing experiments only (env LFEM_DEBUG_TILED): bit0 compute skips the kinds, bit1 reduce skips the slots,
-                //   bit2 per-role phase cycles -> dbg[16]
-    unsigned long long* dbg;
 };
 
 extern __shared__ __align__(16) double tile_smem_d[];  // dynamic shared memory (one view per TU)
@@ -300,6 +290,9 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
     const int G = gridDim.x;
     const TileLayout lay = tile_layout(E::NS, N, a.maxe, a.slots_cap, a.heavy_cap, a.nodes_cap);
     const int stage_dbl = (int)(lay.stage_bytes / sizeof(double));
+    // buffer bases by arithmetic (a dynamically indexed member array would live in local memory)
+    const size_t meta0 = lay.meta_off[0], meta_stride = lay.meta_off[1] - lay.meta_off[0];
+    const size_t node0 = lay.node_off[0], node_stride = lay.node_off[1] - lay.node_off[0];
 
     if (tid == 0) {
         for (int b = 0; b < 3; ++b) {
@@ -329,24 +322,20 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
         if (Cfg::REGS_C) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_C));
         int t = blockIdx.x;
         if (t >= a.n_tiles) return;
-        PhaseClock pc{(a.debug & 4) != 0 && tid == 0, 0};
-        pc.start();
         double X[EPT][N][3], U[EPT][N];
         uint32_t pass = 0;
         mbar_wait(&meta_full[0], 0);
-        prefetch_tile_nodes(a, DAA, sinfo[0][2],
-                            reinterpret_cast<const int32_t*>(smem + lay.meta_off[0] + lay.halo_off),
-                            smem + lay.node_off[0], lay, &node_full[0], tid, CT);
+        prefetch_tile_nodes(a, DAA, sinfo[0][2], reinterpret_cast<const int32_t*>(smem + meta0 + lay.halo_off),
+                            smem + node0, lay, &node_full[0], tid, CT);
         for (int it = 0; t < a.n_tiles; ++it, t += G) {
             const int b = it % 3, nb = it & 1;
             const int4 i0 = sinfo[b][0], i2 = sinfo[b][2];
             const int e0 = i0.z, ne = i0.w;
             // this tile's node buffer: bulk copies + every thread's halo gathers, one mbarrier
             mbar_wait(&node_full[nb], (it >> 1) & 1);
-            read_nodes<F, DAA, EPT>(i2, reinterpret_cast<const uint16_t*>(smem + lay.meta_off[b] + lay.conn_off),
-                                    smem + lay.node_off[nb], lay, ne, tid, CT, X, U);
+            read_nodes<F, DAA, EPT>(i2, reinterpret_cast<const uint16_t*>(smem + meta0 + b * meta_stride + lay.conn_off),
+                                    smem + node0 + nb * node_stride, lay, ne, tid, CT, X, U);
             mbar_arrive(&node_empty[nb]);
-            pc.lap(a.dbg, 0);  // loop overhead / meta wait (no PRE) / prefetched nodes
             typename E::Geo geo[EPT];
 #pragma unroll
             for (int k = 0; k < EPT; ++k) {
@@ -354,126 +343,94 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 if (e < ne && !E::template geometry<DAA>(X[k], U[k], geo[k]))
                     atomicMin(a.err, __ldg(&a.elem_list[__ldg(&a.tile_elems[e0 + e])]));
             }
-            pc.lap(a.dbg, 1);  // geometry (incl. waiting for the prefetched nodes)
             if (t + G < a.n_tiles) {  // next tile's nodes -> the other node buffer, in flight during the kinds
                 const int bn = (it + 1) % 3;
                 mbar_wait(&meta_full[bn], ((it + 1) / 3) & 1);
                 const int fill = (it + 1) >> 1;  // fill index of buffer nb ^ 1: its previous contents must be read
                 if (fill > 0) mbar_wait(&node_empty[nb ^ 1], (fill - 1) & 1);
-                pc.lap(a.dbg, 2);  // wait for the next tile's metadata
                 prefetch_tile_nodes(a, DAA, sinfo[bn][2],
-                                    reinterpret_cast<const int32_t*>(smem + lay.meta_off[bn] + lay.halo_off),
-                                    smem + lay.node_off[nb ^ 1], lay, &node_full[nb ^ 1], tid, CT);
+                                    reinterpret_cast<const int32_t*>(smem + meta0 + bn * meta_stride + lay.halo_off),
+                                    smem + node0 + (nb ^ 1) * node_stride, lay, &node_full[nb ^ 1], tid, CT);
             }
             // one kind per stage pass: wait for a free stage buffer, store, hand it to the reduce warps
-#define LFEM_STAGE_ACQUIRE()                                                   \
-    const int sb_ = pass % LFEM_NSB;                                           \
-    const uint32_t use_ = pass / LFEM_NSB;                                     \
-    pc.lap(a.dbg, 3);                                                          \
-    if (use_ > 0) mbar_wait(&stage_empty[sb_], (use_ - 1) & 1);                \
-    pc.lap(a.dbg, 4);                                                          \
-    double* st = tile_smem_d + sb_ * stage_dbl;                                \
-    const bool do_store = !(a.debug & 1)
-#define LFEM_STAGE_RELEASE()              \
-    mbar_arrive(&stage_full[sb_]);        \
-    pc.lap(a.dbg, 5);                     \
-    ++pass
-            if (DM) {
-                LFEM_STAGE_ACQUIRE();
-#pragma unroll
-                for (int k = 0; k < EPT; ++k) {
-                    const int e = tid + k * CT;
-                    if (e < ne && do_store) {
-                        StageSink sink{st, a.maxe, e};
-                        E::template kind<KIND_M>(geo[k], sink);
-                    }
-                }
-                LFEM_STAGE_RELEASE();
-            }
-            {
-                if (DA) {
-                    LFEM_STAGE_ACQUIRE();
-#pragma unroll
-                    for (int k = 0; k < EPT; ++k) {
-                        const int e = tid + k * CT;
-                        if (e < ne && do_store) {
-                            StageSink sink{st, a.maxe, e};
-                            E::template kind<KIND_A>(geo[k], sink);
-                        }
-                    }
-                    LFEM_STAGE_RELEASE();
-                }
-                if (DAA) {
-                    LFEM_STAGE_ACQUIRE();
-#pragma unroll
-                    for (int k = 0; k < EPT; ++k) {
-                        const int e = tid + k * CT;
-                        if (e < ne && do_store) {
-                            StageSink sink{st, a.maxe, e};
-                            E::template kind<KIND_AA>(geo[k], sink);
-                        }
-                    }
-                    LFEM_STAGE_RELEASE();
-                }
-            }
-#undef LFEM_STAGE_ACQUIRE
-#undef LFEM_STAGE_RELEASE
-        }
-    } else {
-        // ------------------------------------------------------------ reduce warps (+ producer)
-        if (Cfg::REGS_R) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_R));
-        const int rw = warp - CW;
-        uint32_t pass = 0;
-        PhaseClock pc{(a.debug & 4) != 0 && tid == CT, 0};
-        pc.start();
-        for (int it = 0, t = blockIdx.x; t < a.n_tiles; ++it, t += G) {
-            const int b = it % 3;
-            pc.lap(a.dbg, 8);  // misc
-            mbar_wait(&meta_full[b], (it / 3) & 1);
-            pc.lap(a.dbg, 9);  // wait for metadata
-            const int4 i0 = sinfo[b][0], i1 = sinfo[b][1];
-            const int s0 = i0.x, ns = i0.y;
-            const uint32_t* s_pairs =
-                reinterpret_cast<const uint32_t*>(smem + lay.meta_off[b] + lay.pairs_off) + (s0 & 3);
-            const int hw = a.heavy_words, nent = i1.w / hw;
-            const uint16_t* s_heavy =  // entries start 16-B aligned (h0 is a multiple of hw >= 8)
-                reinterpret_cast<const uint16_t*>(smem + lay.meta_off[b] + lay.heavy_off);
 #pragma unroll
             for (int kind = 0; kind < 3; ++kind) {
                 if ((kind == KIND_M && !DM) || (kind == KIND_A && !DA) || (kind == KIND_AA && !DAA)) continue;
                 const int sb = pass % LFEM_NSB;
-                pc.lap(a.dbg, 8);
-                mbar_wait(&stage_full[sb], (pass / LFEM_NSB) & 1);
-                pc.lap(a.dbg, 10);  // wait for a full stage
-                const double* st = tile_smem_d + sb * stage_dbl;
-                double* out = a.v[kind] + s0;
-                const int ns_eff = (a.debug & 2) ? 0 : ns;
-                // light slots (1-2 contributions): UR 32-slot chunks per iteration (independent load chains)
-                constexpr int UR = Cfg::RU;
-                for (int j0 = rw * 32; j0 < ns_eff; j0 += UR * RW * 32) {
-                    uint32_t pw[UR];
+                const uint32_t use = pass / LFEM_NSB;
+                if (use > 0) mbar_wait(&stage_empty[sb], (use - 1) & 1);
+                double* st = tile_smem_d + sb * stage_dbl;
 #pragma unroll
-                    for (int u = 0; u < UR; ++u) {
-                        const int j = j0 + u * RW * 32 + lane;
-                        pw[u] = j < ns_eff ? s_pairs[j] : 0xffffffffu;
-                    }
-                    double x0[UR], x1[UR];
-#pragma unroll
-                    for (int u = 0; u < UR; ++u) {
-                        const uint32_t c0 = pw[u] & 0xffffu, c1 = pw[u] >> 16;
-                        x0[u] = c0 != 0xffffu ? st[c0] : 0.0;
-                        x1[u] = c1 != 0xffffu ? st[c1] : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < UR; ++u) {
-                        // (0 + x0) + x1: the order of V0 and the oracle; + 0.0 is exact (sums are never -0)
-                        const double v = (0.0 + x0[u]) + x1[u];
-                        if (pw[u] != 0xffffffffu) st_stream(out + j0 + u * RW * 32 + lane, v);
+                for (int k = 0; k < EPT; ++k) {
+                    const int e = tid + k * CT;
+                    if (e < ne && !(LFEM_TILED_SKIP & 1)) {
+                        StageSink sink{st, a.maxe, e};
+                        if (kind == KIND_M) E::template kind<KIND_M>(geo[k], sink);
+                        else if (kind == KIND_A) E::template kind<KIND_A>(geo[k], sink);
+                        else E::template kind<KIND_AA>(geo[k], sink);
                     }
                 }
-                pc.lap(a.dbg, 11);  // light slots
-                // heavy slots: one fixed-size entry per lane, loads in parallel, summed in order
-                for (int h = rw * 32 + lane; h < ((a.debug & 2) ? 0 : nent); h += RW * 32) {
+                mbar_arrive(&stage_full[sb]);
+                ++pass;
+            }
+        }
+    } else {
+        // ------------------------------------------------------------ reduce warps (+ producer)
+        // Light slots (1-2 contributions) in units of two consecutive CSR slots (absolute
+        // index 2u, 2u+1): one 8-B load of the two slot words, four stage loads, one
+        // 16-B streaming store; consecutive threads take consecutive units (512-B
+        // coalesced stores per warp).  Slot words hold stage BYTE offsets.  One compact
+        // loop serves every kind (the kinds' code is not replicated: instruction-cache
+        // footprint).  Heavy entries: one per thread, loads in parallel, summed in order.
+        if (Cfg::REGS_R) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_R));
+        constexpr int RT = RW * 32;
+        constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
+        const int rw = warp - CW, rt = tid - CT;
+        (void)rw;
+        uint32_t pass = 0;
+        for (int it = 0, t = blockIdx.x; t < a.n_tiles; ++it, t += G) {
+            const int b = it % 3;
+            mbar_wait(&meta_full[b], (it / 3) & 1);
+            const int4 i0 = sinfo[b][0], i1 = sinfo[b][1];
+            const int s0 = i0.x, ns = (LFEM_TILED_SKIP & 2) ? 0 : i0.y, se = s0 + ns;
+            const unsigned char* mb = smem + meta0 + b * meta_stride;
+            // slot words of absolute slots [p0, ...), p0 = s0 & ~3 (16-B aligned bulk copy)
+            const uint32_t* s_pw = reinterpret_cast<const uint32_t*>(mb + lay.pairs_off);
+            const int p0 = s0 & ~3;
+            const int hw = a.heavy_words, nent = (LFEM_TILED_SKIP & 2) ? 0 : i1.w / hw;
+            const uint16_t* s_heavy = reinterpret_cast<const uint16_t*>(mb + lay.heavy_off);
+            const int u0 = s0 >> 1, u1 = (se + 1) >> 1;
+#pragma unroll 1
+            for (int kk = 0; kk < NK; ++kk) {
+                const int kind = DM ? (kk == 0 ? KIND_M : (DA && kk == 1) ? KIND_A : KIND_AA)
+                                    : (DA ? (kk == 0 ? KIND_A : KIND_AA) : KIND_AA);
+                const int sb = pass % LFEM_NSB;
+                mbar_wait(&stage_full[sb], (pass / LFEM_NSB) & 1);
+                const unsigned char* st = reinterpret_cast<const unsigned char*>(tile_smem_d + sb * stage_dbl);
+                double* out = a.v[kind];
+#pragma unroll 2
+                for (int u = u0 + rt; u < u1; u += RT) {
+                    const int sa = 2 * u;
+                    const uint2 w = *reinterpret_cast<const uint2*>(s_pw + (sa - p0));
+                    // a word outside the tile's range, or a heavy slot, is not written here
+                    const bool ok0 = sa >= s0 && w.x != 0xffffffffu;
+                    const bool ok1 = sa + 1 < se && w.y != 0xffffffffu;
+                    const uint32_t a0 = w.x & 0xffffu, b0 = w.x >> 16, a1 = w.y & 0xffffu, b1 = w.y >> 16;
+                    const double x00 = ok0 ? *reinterpret_cast<const double*>(st + a0) : 0.0;
+                    const double x01 = ok0 && b0 != 0xffffu ? *reinterpret_cast<const double*>(st + b0) : 0.0;
+                    const double x10 = ok1 ? *reinterpret_cast<const double*>(st + a1) : 0.0;
+                    const double x11 = ok1 && b1 != 0xffffu ? *reinterpret_cast<const double*>(st + b1) : 0.0;
+                    // (0 + x0) + x1: the order of V0 and the oracle; + 0.0 is exact (sums are never -0)
+                    const double v0 = (0.0 + x00) + x01, v1 = (0.0 + x10) + x11;
+                    if (ok0 && ok1) {
+                        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(out + sa), "d"(v0), "d"(v1) : "memory");
+                    } else {
+                        if (ok0) st_stream(out + sa, v0);
+                        if (ok1) st_stream(out + sa + 1, v1);
+                    }
+                }
+                // heavy slots: one fixed-size entry per thread, loads in parallel, summed in order
+                for (int h = rt; h < nent; h += RT) {
                     const uint4* ent = reinterpret_cast<const uint4*>(s_heavy + h * hw);
                     const uint4 w0 = ent[0];
                     const int cnt = (int)(w0.x >> 16);
@@ -481,7 +438,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                                            w0.w & 0xffffu, w0.w >> 16};
                     double x[6];
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) x[k] = c[k] != 0xffffu ? st[c[k]] : 0.0;
+                    for (int k = 0; k < 6; ++k) x[k] = c[k] != 0xffffu ? *reinterpret_cast<const double*>(st + c[k]) : 0.0;
                     double v = 0.0;
 #pragma unroll
                     for (int k = 0; k < 6; ++k) v = v + x[k];
@@ -491,13 +448,13 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                                                w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
                         double y[8];
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) y[k] = d[k] != 0xffffu ? st[d[k]] : 0.0;
+                        for (int k = 0; k < 8; ++k)
+                            y[k] = d[k] != 0xffffu ? *reinterpret_cast<const double*>(st + d[k]) : 0.0;
 #pragma unroll
                         for (int k = 0; k < 8; ++k) v = v + y[k];
                     }
-                    st_stream(out + (w0.x & 0xffffu), v);
+                    st_stream(out + s0 + (w0.x & 0xffffu), v);
                 }
-                pc.lap(a.dbg, 12);  // heavy slots
                 mbar_arrive(&stage_empty[sb]);
                 ++pass;
             }
@@ -509,9 +466,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 if (done == RW - 1) {
                     meta_done[b] = 0;
                     __threadfence_block();
-                    pc.lap(a.dbg, 8);
                     if (t + 3 * G < a.n_tiles) issue_tile(a, smem, lay, t + 3 * G, b, sinfo, meta_full);
-                    pc.lap(a.dbg, 13);  // producer
                 }
             }
         }
@@ -533,15 +488,13 @@ size_t tile_smem_bytes(const TilePlan& T) {
 // Build the tile plan with an element budget of the compute threads' capacity
 // (or LFEM_TILE_ELEMS), lowered if the 16-bit codes or shared memory do not fit.
 template <int F>
-lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
+lfem_status ensure_tiles_impl(lfem_plan_s* p, cudaStream_t s) {
     TilePlan& T = p->tiles;
-    if (T.ready) return LFEM_OK;
     int emax = tile_capacity<F>();
     // tiny meshes (fewer elements than ~2 full tiles per SM): smaller tiles spread them over the SMs
     // (a tile's pipeline latency, not its work, sets the time there)
-    int dev = 0, sms = 148;
-    LFEM_CUDA(cudaGetDevice(&dev));
-    LFEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    int sms = 148;
+    LFEM_TRY(device_sm_count(&sms));
     if (p->n_local < (int64_t)emax * sms * 2) {
         const int64_t e = (p->n_local + sms - 1) / sms;
         emax = (int)(e < 32 ? 32 : (e > emax ? emax : e));
@@ -561,6 +514,22 @@ lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
     return LFEM_OK;
 }
 
+// the tile plan is built once per plan; a failed build leaves no plan behind
+// (tiled_ok = 0: AUTO runs V0 on this plan from then on)
+template <int F>
+lfem_status ensure_tiles(lfem_plan_s* p, cudaStream_t s) {
+    if (p->tiles.ready && p->tiled_ok == 1) return LFEM_OK;
+    if (p->tiled_ok == 0) return lfem_fail(LFEM_ERR_UNSUPPORTED, "the tile plan does not fit this mesh");
+    const lfem_status st = ensure_tiles_impl<F>(p, s);
+    if (st != LFEM_OK) {
+        free_tiles(p->tiles, s);
+        if (st == LFEM_ERR_UNSUPPORTED) p->tiled_ok = 0;
+        return st;
+    }
+    p->tiled_ok = 1;
+    return LFEM_OK;
+}
+
 template <int F, bool DM, bool DA, bool DAA>
 lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff, double* const vals[3],
                       cudaStream_t s) {
@@ -569,18 +538,9 @@ lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff,
     if (T.n_tiles == 0) return LFEM_OK;
     const size_t smem = tile_smem_bytes<F>(T);
     constexpr int THREADS = (TileCfg<F>::CW + TileCfg<F>::RW) * 32;
-    static int attr_smem = -1;  // per instantiation; one process drives one device
-    if (attr_smem < (int)smem) {
-        LFEM_CUDA(cudaFuncSetAttribute(k_tiled<F, DM, DA, DAA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem));
-        attr_smem = (int)smem;
-    }
-    static int sm_count = 0;
-    if (sm_count == 0) {
-        int dev = 0;
-        LFEM_CUDA(cudaGetDevice(&dev));
-        LFEM_CUDA(cudaDeviceGetAttribute(&sm_count, cudaDevAttrMultiProcessorCount, dev));
-    }
+    LFEM_TRY(ensure_smem_attr(reinterpret_cast<const void*>(k_tiled<F, DM, DA, DAA>), (int)smem));
+    int sm_count = 148;
+    LFEM_TRY(device_sm_count(&sm_count));
     int occ = 0;
     LFEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<F, DM, DA, DAA>, THREADS, smem));
     if (occ < 1) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tiled kernel does not fit on an SM");
@@ -603,31 +563,11 @@ lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff,
     a.coeff = coeff;
     for (int k = 0; k < 3; ++k) a.v[k] = vals[k];
     a.err = p->err;
-    a.debug = 0;
-    a.dbg = nullptr;
-    if (const char* env = std::getenv("LFEM_DEBUG_TILED")) a.debug = std::atoi(env);
-    static unsigned long long* dbg = nullptr;
-    if (a.debug & 4) {
-        if (!dbg) LFEM_TRY(dev_alloc_t(&dbg, 16, s));
-        LFEM_CUDA(cudaMemsetAsync(dbg, 0, 16 * sizeof(unsigned long long), s));
-        a.dbg = dbg;
-    }
     const int grid = T.n_tiles < occ * sm_count ? T.n_tiles : occ * sm_count;
     prof_begin(p, "k_tiled", s);
     k_tiled<F, DM, DA, DAA><<<grid, THREADS, smem, s>>>(a);
     LFEM_CUDA(cudaGetLastError());
     prof_end(p, s);
-    if (a.debug & 4) {  // per-CTA average cycles per phase (one thread per role)
-        unsigned long long h[16];
-        LFEM_CUDA(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, s));
-        LFEM_CUDA(cudaStreamSynchronize(s));
-        std::fprintf(stderr, "[tiled phases, kcycles/CTA] grid %d tiles %d R %d maxe %d | compute: misc %.0f geo %.0f "
-                     "meta %.0f pre %.0f wait_stage %.0f kinds %.0f | reduce: misc %.0f meta %.0f wait_stage %.0f "
-                     "light %.0f heavy %.0f producer %.0f\n", grid, T.n_tiles, T.rows_per_tile, T.max_tile_elems,
-                     h[0] / 1e3 / grid, h[1] / 1e3 / grid, h[2] / 1e3 / grid, h[3] / 1e3 / grid, h[4] / 1e3 / grid,
-                     h[5] / 1e3 / grid, h[8] / 1e3 / grid, h[9] / 1e3 / grid, h[10] / 1e3 / grid, h[11] / 1e3 / grid,
-                     h[12] / 1e3 / grid, h[13] / 1e3 / grid);
-    }
     return LFEM_OK;
 }
 

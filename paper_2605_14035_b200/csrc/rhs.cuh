@@ -405,14 +405,9 @@ lfem_status run_rhs_tiled(lfem_plan_s* p, const double* coords, const double* u,
     if (T.n_tiles == 0) return LFEM_OK;
     constexpr int SBD = (FamInfo<F>::NREF * RhsInfo<KIND>::NC) | 1;
     const size_t smem = (size_t)T.max_tile_count * SBD * sizeof(double);
-    static int attr_smem = -1;  // per instantiation
-    if (attr_smem < (int)smem) {
-        LFEM_CUDA(cudaFuncSetAttribute(k_rhs_tiled<F, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_smem = (int)smem;
-    }
-    int dev = 0, sms = 148, occ = 0;
-    LFEM_CUDA(cudaGetDevice(&dev));
-    LFEM_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    LFEM_TRY(ensure_smem_attr(reinterpret_cast<const void*>(k_rhs_tiled<F, KIND>), (int)smem));
+    int sms = 148, occ = 0;
+    LFEM_TRY(device_sm_count(&sms));
     LFEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_rhs_tiled<F, KIND>, RHS_THREADS, smem));
     if (occ < 1) return lfem_fail(LFEM_ERR_UNSUPPORTED, "fused right-hand side kernel does not fit on an SM");
     const int grid = T.n_tiles < occ * sms ? T.n_tiles : occ * sms;
@@ -443,12 +438,7 @@ lfem_status run_rhs(lfem_plan_s* p, const double* coords, const double* u, doubl
     if (p->n_local > 0) {
         prof_begin(p, "k_rhs_elem", s);
         constexpr size_t smem = sizeof(double) * (size_t)RHS_THREADS * BD;
-        static bool attr = false;  // per instantiation
-        if (!attr) {
-            LFEM_CUDA(cudaFuncSetAttribute(k_rhs_elem<F, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)smem));
-            attr = true;
-        }
+        LFEM_TRY(ensure_smem_attr(reinterpret_cast<const void*>(k_rhs_elem<F, KIND>), (int)smem));
         k_rhs_elem<F, KIND><<<grid_for(p->n_local, RHS_THREADS, 1 << 20), RHS_THREADS, smem, s>>>(
             p->n_local, p->local_conn, p->elem_list, coords, u, p->mesh->n_nodes, p->rhs_stage, p->err);
         LFEM_CUDA(cudaGetLastError());

@@ -87,9 +87,12 @@ lfem_status scan_impl(const T* in, int64_t* out, int64_t n, cudaStream_t s) {
         return LFEM_OK;
     }
     const int64_t tiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    DevScope scope(s);  // both temporaries are freed on every exit path
     int64_t* tile_sums = nullptr;
-    LFEM_TRY(dev_alloc_t(&tile_sums, tiles + 1, s));
+    scope.track(&tile_sums);
     int64_t* tile_offsets = nullptr;
+    scope.track(&tile_offsets);
+    LFEM_TRY(dev_alloc_t(&tile_sums, tiles + 1, s));
     LFEM_TRY(dev_alloc_t(&tile_offsets, tiles + 1, s));
     k_tile_reduce<T><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, tile_sums);
     LFEM_CUDA(cudaGetLastError());
@@ -101,8 +104,6 @@ lfem_status scan_impl(const T* in, int64_t* out, int64_t n, cudaStream_t s) {
     }
     k_tile_scan<T><<<(unsigned)tiles, SCAN_THREADS, 0, s>>>(in, n, tile_offsets, out);
     LFEM_CUDA(cudaGetLastError());
-    dev_free(tile_sums, s);
-    dev_free(tile_offsets, s);
     return LFEM_OK;
 }
 

@@ -19,6 +19,7 @@
 //   4. k_row_pattern<1>: col_idx (ascending) and the reduction plan: for
 //      every CSR slot the list of its contributions (e, a, b) in ascending
 //      (e, a, b) order (slot_ptr + codes, code = e_local * nsym + sym(a,b)).
+#include <algorithm>
 #include <climits>
 #include <vector>
 
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(ROW_WARPS * 32)
 k_row_pattern(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ inc, int64_t n_rows,
               const int32_t* __restrict__ lconn, int nref, int nsym, int32_t* __restrict__ row_len,
               const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx, int32_t* __restrict__ slot_ptr,
-              int32_t* __restrict__ codes, int* __restrict__ overflow) {
+              int32_t* __restrict__ codes, int* __restrict__ nbig, int32_t* __restrict__ big, int big_cap) {
     __shared__ int32_t s_col[ROW_WARPS][MAX_CAND];
     __shared__ int32_t s_src[ROW_WARPS][MAX_CAND];  // e_local * nref + a  (PASS 1)
     __shared__ uint8_t s_first[ROW_WARPS][MAX_CAND];
@@ -107,9 +108,12 @@ k_row_pattern(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ i
     for (int64_t r = blockIdx.x * (int64_t)ROW_WARPS + warp; r < n_rows; r += nwarps) {
         const int64_t ib = inc_ptr[r], ie = inc_ptr[r + 1];
         const int nc = (int)((ie - ib) * nref);
-        if (nc > MAX_CAND) {
-            if (lane == 0) atomicExch(overflow, 1);
-            if (PASS == 0 && lane == 0) row_len[r] = 0;
+        if (nc > MAX_CAND) {  // long row: k_row_big (one CTA per row, global scratch)
+            if (PASS == 0 && lane == 0) {
+                row_len[r] = 0;
+                const int k = atomicAdd(nbig, 1);
+                if (k < big_cap) big[k] = (int32_t)r;
+            }
             continue;
         }
         for (int i = lane; i < nc; i += 32) {
@@ -161,6 +165,81 @@ k_row_pattern(const int64_t* __restrict__ inc_ptr, const int32_t* __restrict__ i
             }
         }
         __syncwarp();
+    }
+}
+
+// Rows with more than MAX_CAND candidates (e.g. a vertex shared by more than 51 P2
+// tetrahedra): the same computation as k_row_pattern, one CTA per row, candidates in a
+// global scratch range [off[k], off[k+1]) of the k-th long row.
+constexpr int BIG_THREADS = 256;
+
+__global__ void k_big_nc(const int32_t* __restrict__ big, int nbig, const int64_t* __restrict__ inc_ptr, int nref,
+                         int64_t* __restrict__ nc) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < nbig; k += gridDim.x * blockDim.x)
+        nc[k] = (inc_ptr[big[k] + 1] - inc_ptr[big[k]]) * nref;
+}
+
+template <int PASS>
+__global__ void __launch_bounds__(BIG_THREADS)
+k_row_big(const int32_t* __restrict__ big, const int64_t* __restrict__ off, const int64_t* __restrict__ inc_ptr,
+          const int32_t* __restrict__ inc, const int32_t* __restrict__ lconn, int nref, int nsym,
+          int32_t* __restrict__ row_len, const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col_idx,
+          int32_t* __restrict__ slot_ptr, int32_t* __restrict__ codes, int32_t* __restrict__ g_col,
+          int32_t* __restrict__ g_src, uint8_t* __restrict__ g_first) {
+    __shared__ int s_red[BIG_THREADS / 32];
+    const int64_t r = big[blockIdx.x];
+    const int64_t ib = inc_ptr[r], base = off[blockIdx.x];
+    const int nc = (int)(off[blockIdx.x + 1] - base);
+    int32_t* col = g_col + base;
+    int32_t* src_ = g_src + base;
+    uint8_t* first = g_first + base;
+    for (int i = threadIdx.x; i < nc; i += BIG_THREADS) {
+        const int k = i / nref, b = i - k * nref;
+        const int32_t src = inc[ib + k];
+        col[i] = lconn[(int64_t)(src / nref) * nref + b];
+        src_[i] = src;
+    }
+    __syncthreads();
+    int nfirst = 0;
+    for (int i = threadIdx.x; i < nc; i += BIG_THREADS) {
+        const int32_t c = col[i];
+        bool f = true;
+        for (int j = 0; j < i && f; ++j) f = col[j] != c;
+        first[i] = f;
+        nfirst += f;
+    }
+    if (PASS == 0) {
+        for (int o = 16; o > 0; o >>= 1) nfirst += __shfl_down_sync(0xffffffffu, nfirst, o);
+        if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = nfirst;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int w = 0; w < BIG_THREADS / 32; ++w) t += s_red[w];
+            row_len[r] = t;
+        }
+        return;
+    }
+    __syncthreads();
+    const int64_t rp = row_ptr[r];
+    const int64_t cbase = ib * nref;
+    for (int i = threadIdx.x; i < nc; i += BIG_THREADS) {
+        const int32_t c = col[i];
+        int less = 0, less_unique = 0, before_eq = 0;
+        for (int j = 0; j < nc; ++j) {
+            const int32_t cj = col[j];
+            less += (cj < c);
+            less_unique += (cj < c) & first[j];
+            before_eq += (cj == c) & (j < i);
+        }
+        if (first[i]) {
+            col_idx[rp + less_unique] = c;
+            slot_ptr[rp + less_unique] = (int32_t)(cbase + less);
+        }
+        const int32_t src = src_[i];
+        const int32_t le = src / nref;
+        const int a = src - le * nref;
+        const int b = i - (i / nref) * nref;
+        codes[cbase + less + before_eq] = (int32_t)((int64_t)le * nsym + sym_index(nref, a, b));
     }
 }
 
@@ -265,25 +344,67 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     int32_t* cnt = nullptr;
     scope.track(&cnt);
     LFEM_TRY(dev_alloc_t(&cnt, n_rows + 1, s));
-    // 3. row lengths
-    int* overflow = nullptr;
-    scope.track(&overflow);
-    LFEM_TRY(dev_alloc_t(&overflow, 1, s));
-    LFEM_CUDA(cudaMemsetAsync(overflow, 0, sizeof(int), s));
+    // 3. row lengths (rows with more than MAX_CAND candidates go to k_row_big)
+    constexpr int BIG_CAP = 1 << 16;
+    int* nbig_d = nullptr;
+    scope.track(&nbig_d);
+    int32_t* big = nullptr;
+    scope.track(&big);
+    LFEM_TRY(dev_alloc_t(&nbig_d, 1, s));
+    LFEM_TRY(dev_alloc_t(&big, BIG_CAP, s));
+    LFEM_CUDA(cudaMemsetAsync(nbig_d, 0, sizeof(int), s));
     const unsigned rgrid = grid_for(n_rows, ROW_WARPS);
     if (n_rows > 0) {
         k_row_pattern<0><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, m->nsym, cnt,
-                                                          nullptr, nullptr, nullptr, nullptr, overflow);
+                                                          nullptr, nullptr, nullptr, nullptr, nbig_d, big, BIG_CAP);
         LFEM_CUDA(cudaGetLastError());
+    }
+    int nbig = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&nbig, nbig_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    if (nbig > BIG_CAP)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "more than 65536 rows with > 512 candidate (element, column) entries");
+    int64_t* big_off = nullptr;
+    scope.track(&big_off);
+    int32_t *g_col = nullptr, *g_src = nullptr;
+    uint8_t* g_first = nullptr;
+    scope.track(&g_col);
+    scope.track(&g_src);
+    scope.track(&g_first);
+    if (nbig > 0) {
+        // the long rows' candidate counts -> scratch offsets (host; long rows are rare)
+        std::vector<int32_t> hbig(nbig);
+        LFEM_CUDA(cudaMemcpyAsync(hbig.data(), big, sizeof(int32_t) * nbig, cudaMemcpyDeviceToHost, s));
+        LFEM_CUDA(cudaStreamSynchronize(s));
+        std::sort(hbig.begin(), hbig.end());
+        LFEM_CUDA(cudaMemcpyAsync(big, hbig.data(), sizeof(int32_t) * nbig, cudaMemcpyHostToDevice, s));
+        LFEM_TRY(dev_alloc_t(&big_off, (size_t)nbig + 1, s));
+        k_big_nc<<<grid_for(nbig, 256), 256, 0, s>>>(big, nbig, inc_ptr, nref, big_off);
+        LFEM_CUDA(cudaGetLastError());
+        std::vector<int64_t> hoff(nbig + 1, 0);
+        LFEM_CUDA(cudaMemcpyAsync(hoff.data(), big_off, sizeof(int64_t) * nbig, cudaMemcpyDeviceToHost, s));
+        LFEM_CUDA(cudaStreamSynchronize(s));
+        int64_t run = 0;
+        for (int k = 0; k < nbig; ++k) {
+            const int64_t c = hoff[k];
+            if (c >= (int64_t)INT_MAX) return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row has >= 2^31 candidates");
+            hoff[k] = run;
+            run += c;
+        }
+        hoff[nbig] = run;
+        LFEM_CUDA(cudaMemcpyAsync(big_off, hoff.data(), sizeof(int64_t) * (nbig + 1), cudaMemcpyHostToDevice, s));
+        LFEM_TRY(dev_alloc_t(&g_col, (size_t)run + 1, s));
+        LFEM_TRY(dev_alloc_t(&g_src, (size_t)run + 1, s));
+        LFEM_TRY(dev_alloc_t(&g_first, (size_t)run + 1, s));
+        k_row_big<0><<<nbig, BIG_THREADS, 0, s>>>(big, big_off, inc_ptr, inc, p->local_conn, nref, m->nsym, cnt,
+                                                  nullptr, nullptr, nullptr, nullptr, g_col, g_src, g_first);
+        LFEM_CUDA(cudaGetLastError());
+        LFEM_CUDA(cudaStreamSynchronize(s));  // hbig / hoff (pageable) are read by the copies above
     }
     LFEM_TRY(dev_alloc_t(&p->row_ptr, n_rows + 1, s));
     LFEM_TRY(scan_exclusive_i32_to_i64(cnt, p->row_ptr, n_rows, s));
-    int h_overflow = 0;
     LFEM_CUDA(cudaMemcpyAsync(&p->nnz, p->row_ptr + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    LFEM_CUDA(cudaMemcpyAsync(&h_overflow, overflow, sizeof(int), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
-    if (h_overflow)
-        return lfem_fail(LFEM_ERR_UNSUPPORTED, "a row has more than 512 candidate (element, column) entries");
     if (p->nnz >= (int64_t)INT_MAX) return lfem_fail(LFEM_ERR_UNSUPPORTED, "nnz >= 2^31");
     // 4. columns + reduction plan
     LFEM_TRY(dev_alloc_t(&p->col_idx, p->nnz + 1, s));
@@ -292,7 +413,13 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     if (n_rows > 0) {
         k_row_pattern<1><<<rgrid, ROW_WARPS * 32, 0, s>>>(inc_ptr, inc, n_rows, p->local_conn, nref, m->nsym,
                                                           nullptr, p->row_ptr, p->col_idx, p->slot_ptr, p->codes,
-                                                          overflow);
+                                                          nbig_d, big, 0);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    if (nbig > 0) {
+        k_row_big<1><<<nbig, BIG_THREADS, 0, s>>>(big, big_off, inc_ptr, inc, p->local_conn, nref, m->nsym, nullptr,
+                                                  p->row_ptr, p->col_idx, p->slot_ptr, p->codes, g_col, g_src,
+                                                  g_first);
         LFEM_CUDA(cudaGetLastError());
     }
     k_set_last<<<1, 1, 0, s>>>(p->slot_ptr, p->nnz, p->n_contrib);
@@ -300,7 +427,6 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
     scope.drop(cnt);
     scope.drop(inc_ptr);
     scope.drop(inc);
-    scope.drop(overflow);
     LFEM_CUDA(cudaStreamSynchronize(s));
     return LFEM_OK;
 }

@@ -16,8 +16,8 @@
 // every segment start), so it is parallel and deterministic.
 //
 // Reduction codes.  A contribution (e, a, b) of the symbolic plan becomes the
-// 16-bit stage address  code = sym(a,b) * maxe + e_tile  (maxe = max tile
-// elements = stage stride).  Every slot keeps its contributions in symbolic
+// 16-bit stage byte offset  code = 8 * (sym(a,b) * maxe + e_tile)  (maxe = max
+// tile elements = stage stride; byte offsets save the kernel an address shift).  Every slot keeps its contributions in symbolic
 // order (ascending element, then (a, b): reading G21) and is described by one
 // 32-bit word:
 //   1 or 2 contributions  (c0, c1)   c1 = 0xffff if there is one
@@ -212,7 +212,7 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
                     if (te[mid] < le) lo = mid + 1; else hi = mid;
                 }
                 if (lo >= ne || te[lo] != le) atomicExch(bad, 2);
-                const int64_t v = (int64_t)sym * maxe + lo;
+                const int64_t v = 8 * ((int64_t)sym * maxe + lo);
                 if (v >= 0xffff) atomicExch(bad, 4);
                 if (hv) heavy[cur + 2 + (j - j0)] = (uint16_t)v;
                 else code[j - j0] = (uint32_t)v;
@@ -430,6 +430,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     int64_t total = 0;
     LFEM_CUDA(cudaMemcpyAsync(&total, ptr + n_tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     LFEM_CUDA(cudaStreamSynchronize(s));
+    T.total_elems = total;
     LFEM_TRY(dev_alloc_t(&tmp, total + 1, s));
     LFEM_TRY(dev_alloc_t(&T.tile_elems, total + 1, s));
     LFEM_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n_tiles + 1), s));
@@ -451,7 +452,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     const int maxe = (h[1] > 0 ? h[1] : 1) | 1;
     T.max_tile_elems = maxe;
     T.max_tile_count = h[1];
-    if ((int64_t)p->mesh->nsym * maxe >= 0xffff) {  // 16-bit codes: the caller lowers the budget
+    if (8 * (int64_t)p->mesh->nsym * maxe >= 0xffff) {  // 16-bit byte offsets: the caller lowers the budget
         scope.drop(cnt);
         scope.drop(ptr);
         scope.drop(flags);

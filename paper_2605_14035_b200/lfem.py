@@ -37,7 +37,7 @@ EXPORTED = ("lfem_mesh_create", "lfem_mesh_destroy", "lfem_assemble_symbolic", "
             "lfem_numeric_launches", "lfem_error_element", "lfem_last_error", "lfem_version",
             "lfem_profile_enable", "lfem_profile_read", "lfem_set_allocator", "lfem_assemble_rhs",
             "lfem_rhs_ncomp", "lfem_rhs_launches", "lfem_cg_solve", "lfem_mcf_step",
-            "lfem_solve_meanfree")
+            "lfem_solve_meanfree", "lfem_numeric_stats")
 
 
 class LfemError(RuntimeError):
@@ -75,6 +75,7 @@ def _lib():
         L.lfem_plan_check.argtypes = [vp, vp]
         L.lfem_axpby.argtypes = [i64, ctypes.c_double, vp, ctypes.c_double, vp, vp, vp]
         L.lfem_numeric_launches.argtypes = [vp, u32]
+        L.lfem_numeric_stats.argtypes = [vp, ctypes.POINTER(i64), ctypes.POINTER(i64)]
         L.lfem_profile_enable.argtypes = [vp, c_int]
         L.lfem_profile_read.argtypes = [vp, c_int, ctypes.POINTER(ctypes.c_char_p), ctypes.POINTER(ctypes.c_double),
                                         ctypes.POINTER(i64), ctypes.POINTER(c_int)]
@@ -297,6 +298,13 @@ def lfem_numeric_launches(plan: Plan, kinds: int) -> int:
     return int(_lib().lfem_numeric_launches(plan.handle, kinds))
 
 
+def lfem_numeric_stats(plan: Plan):
+    """(element evaluations per numeric call incl. tile halo, row tiles) of the last call."""
+    ev, nt = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib().lfem_numeric_stats(plan.handle, ctypes.byref(ev), ctypes.byref(nt)), "lfem_numeric_stats")
+    return int(ev.value), int(nt.value)
+
+
 def lfem_profile_enable(plan: Plan, enable: bool = True):
     _check(_lib().lfem_profile_enable(plan.handle, 1 if enable else 0), "lfem_profile_enable")
 
@@ -330,16 +338,15 @@ def lfem_set_allocator(alloc=None, dealloc=None) -> None:
 
 
 def torch_caching_allocator():
-    """(alloc, dealloc) pair backed by PyTorch's caching allocator on the current device."""
-    live = {}
-
+    """(alloc, dealloc) pair backed by PyTorch's caching allocator on the current
+    device, stream-ordered on the stream the library hands over (the block is
+    allocated from, and returned to, that stream's pool)."""
     def alloc(n, stream):
-        t = torch.empty(max(int(n), 1), dtype=torch.uint8, device="cuda")
-        live[t.data_ptr()] = t
-        return t.data_ptr()
+        dev = torch.cuda.current_device()
+        return torch.cuda.caching_allocator_alloc(max(int(n), 1), dev, stream or 0)
 
     def dealloc(p, stream):
-        live.pop(int(p), None)
+        torch.cuda.caching_allocator_delete(int(p))
 
     return alloc, dealloc
 

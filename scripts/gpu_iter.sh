@@ -1,8 +1,8 @@
 #!/bin/bash
 # iteration: parity tests (not slow) + benches (CONFIGS x VARIANTS); optional ncu of one config (NCU_CFG)
 cd "$GRAFT_REPO_ROOT"; mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m "gpu and not slow" -x -q ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_gpu.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
-tail -15 gpurun_out/pytest_gpu.log
+timeout 900 python -m pytest tests -m "gpu and not slow" -x -q ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_iter.log 2>&1; echo "pytest exit $?" >> gpurun_out/pytest_iter.log
+tail -15 gpurun_out/pytest_iter.log
 for cfg in ${CONFIGS:-C5 C2 C3}; do
   for v in ${VARIANTS:-auto}; do
     timeout 600 python bench.py --config $cfg --variant $v --steps ${STEPS:-30} --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${cfg}_${v}.json 2> gpurun_out/bench_${cfg}_${v}.log

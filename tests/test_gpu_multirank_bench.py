@@ -46,7 +46,12 @@ def test_two_ranks_match_one(cfg):
     env2 = dict(env, LFEM_BENCH_DEVICE="0", LFEM_BENCH_BACKEND="gloo")
     two = _run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                 "--master-addr", "127.0.0.1", "--master-port", str(_port())] + base[1:] + ["--gpus", "2"], env2)
-    assert two["n_gpus"] == 2 and two["config"]["nnz"] == one["config"]["nnz"]
+    assert two["n_gpus"] == 2 and two["nnz"] == one["nnz"]
+    # per-rank partition report (N > 1): rows and nnz add up, halo elements counted per rank
+    r = two["ranks"]
+    assert sum(r["nnz"]) == one["nnz"] and sum(r["rows"]) == one["config"]["n_nodes"]
+    assert sum(r["n_elems_local"]) >= one["config"]["n_elems"] and r["nnz_spread_max_over_min"] >= 1.0
+    assert one["ranks"] is None
     assert two["gpu_launches"] > 0 and two["value"] > 0
     for k in ("one_M_one", "trace_xAx", "xAx_gathered"):
         a, b = one["verify"][k], two["verify"][k]

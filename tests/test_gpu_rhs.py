@@ -1,10 +1,13 @@
 """GPU parity of the right-hand sides: the CUDA path
 (lfem_assemble_rhs through the C-ABI liblfem.so) against the oracle.
 
-Bar: every entry within 1e-12 x the oracle's sum of |local contributions| of
-that entry (both sides sum the same terms in the same element order; their
-rounding differs only inside the element, by a few ulps of the largest
-term), and exactly 0 where a row has no incident element.
+Bar: every entry within 1e-12 x the oracle's rounding-error scale of that
+entry (reading G33: every quadrature term with |w| mu, |u_h| and |phi| in
+absolute value; for KLL alpha^2 replaced by its first-order error scale
+alpha^2 + 2 sum_k |G_k| B_k, G_k formed from differences on both sides), and
+exactly 0 where a row has no incident element.  On these fields the scale is
+within ~10x of the value (median; test_oracle_rhs.py pins it), so the gate is
+~1e-11 relative.
 """
 import numpy as np
 import pytest

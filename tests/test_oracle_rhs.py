@@ -263,6 +263,34 @@ def test_abs_scale_is_the_value_for_nonnegative_terms():
     assert np.all(babs2 >= np.abs(b2)) and np.any(babs2 > 2 * np.abs(b2))
 
 
+def _kll_test_fields(m, seed):
+    """The GPU parity tests' KLL fields (tests/test_gpu_rhs.py kll_fields)."""
+    x = m.coords
+    r = np.sqrt(np.einsum("ij,ij->i", x, x))
+    nu = (x / r[:, None]).T + 0.05 * np.vstack([li.random_field(m, seed + k) for k in range(3)])
+    H = 2.0 + 0.1 * li.random_field(m, seed + 3)
+    return np.vstack([nu, H[None, :]])
+
+
+@pytest.mark.parametrize("level", [3, 5])
+def test_kll_tolerance_scale_is_tight(level):
+    """Reading G33: the KLL scale is first order in the rounding of alpha^2 = sum_k |G_k|^2
+    (alpha^2 + 2 sum_k |G_k| B_k, G_k from differences), not the square of a running bound.
+    On the parity tests' fields the scale stays within ~10x of the value (median) and 100x
+    (90th percentile), so a 1e-12 x scale gate is a 1e-11..1e-10 relative gate.  With nu = x
+    (alpha^2 = 2 exactly) the scale/value ratio no longer grows like h^-2 with refinement."""
+    m = li.make_config("C5", level_override=level)
+    f, fa = oracle.assemble_rhs_rows(m, _kll_test_fields(m, 5), "kll", with_abs=True)
+    nz = np.abs(f) > 0
+    r = fa[nz] / np.abs(f[nz])
+    assert np.all(fa >= np.abs(f))
+    assert np.median(r) <= 15 and np.percentile(r, 90) <= 100, (np.median(r), np.percentile(r, 90))
+    u = np.vstack([m.coords.T, li.random_field(m, 1)[None, :]])
+    f, fa = oracle.assemble_rhs_rows(m, u, "kll", with_abs=True)
+    nz = np.abs(f) > 0
+    assert np.median(fa[nz] / np.abs(f[nz])) <= 15
+
+
 def test_load_with_dunavant8_on_sphere():
     """The paper's load-vector rule (Dunavant degree 8): on flat P2 elements f_h phi_j has
     degree 4, so the 6-point and 16-point rules agree to rounding; on the curved sphere they differ
