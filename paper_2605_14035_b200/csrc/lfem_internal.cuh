@@ -51,6 +51,7 @@ struct TilePlan {
     int max_tile_heavy = 0;     // max heavy-list u16 words per tile
     int heavy_words = 8;        // u16 words per heavy entry (16-B multiple)
     int32_t* tile_elems = nullptr;      // plan-local element ids, ascending per tile
+    int32_t* tile_elems_pos = nullptr;  // the same ids in stage-position order (tiles.cu k_tile_order)
     int max_tile_nodes = 0;     // max owned rows + halo nodes per tile
     int64_t total_elems = 0;    // element evaluations per numeric call (tile halo included)
     uint16_t* conn16 = nullptr;         // per tile: its elements' tile-local node indices (16-B padded)

@@ -551,7 +551,7 @@ lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff,
     a.heavy_cap = T.max_tile_heavy;
     a.heavy_words = T.heavy_words;
     a.tile_info = T.tile_info;
-    a.tile_elems = T.tile_elems;
+    a.tile_elems = T.tile_elems_pos;  // position order (the compute threads' element index)
     a.conn16 = T.conn16;
     a.halo = T.halo;
     a.nodes_cap = T.max_tile_nodes;

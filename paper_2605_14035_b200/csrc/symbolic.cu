@@ -433,6 +433,7 @@ lfem_status build_symbolic(lfem_plan_s* p, cudaStream_t s) {
 
 void free_tiles(TilePlan& t, cudaStream_t s) {
     dev_free(t.tile_elems, s);
+    dev_free(t.tile_elems_pos, s);
     dev_free(t.conn16, s);
     dev_free(t.halo, s);
     dev_free(t.tile_info, s);

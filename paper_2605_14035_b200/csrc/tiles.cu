@@ -182,8 +182,9 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
                              int hw, int nsym, int maxe,
                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ slot_ptr,
                              const int32_t* __restrict__ codes, const int64_t* __restrict__ tptr,
-                             const int32_t* __restrict__ telems, const int64_t* __restrict__ hptr,
-                             uint32_t* __restrict__ pairs, uint16_t* __restrict__ heavy, int* __restrict__ bad) {
+                             const int32_t* __restrict__ telems, const uint16_t* __restrict__ tpos,
+                             const int64_t* __restrict__ hptr, uint32_t* __restrict__ pairs,
+                             uint16_t* __restrict__ heavy, int* __restrict__ bad) {
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
         const int t = tile_of[r];
         const int32_t* te = telems + tptr[t];
@@ -212,7 +213,7 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
                     if (te[mid] < le) lo = mid + 1; else hi = mid;
                 }
                 if (lo >= ne || te[lo] != le) atomicExch(bad, 2);
-                const int64_t v = 8 * ((int64_t)sym * maxe + lo);
+                const int64_t v = 8 * ((int64_t)sym * maxe + tpos[tptr[t] + lo]);
                 if (v >= 0xffff) atomicExch(bad, 4);
                 if (hv) heavy[cur + 2 + (j - j0)] = (uint16_t)v;
                 else code[j - j0] = (uint32_t)v;
@@ -235,7 +236,7 @@ __global__ void __launch_bounds__(256)
 k_tile_nodes(int n_tiles, int nref, int64_t rb, const int64_t* __restrict__ bounds, const int64_t* __restrict__ ptr,
              const int32_t* __restrict__ telems, const int32_t* __restrict__ lconn, int32_t* __restrict__ hcnt,
              const int32_t* __restrict__ lptr, const int32_t* __restrict__ cptr, int32_t* __restrict__ halo,
-             uint16_t* __restrict__ conn16, int* __restrict__ bad) {
+             uint16_t* __restrict__ conn16, const uint16_t* __restrict__ tpos, int* __restrict__ bad) {
     __shared__ int32_t key[NODE_MAX];
     __shared__ int wsum[8];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -314,11 +315,130 @@ k_tile_nodes(int n_tiles, int nref, int64_t rb, const int64_t* __restrict__ boun
                     loc = nrows + 1 + lo;
                 }
                 if (loc >= 0xffff) atomicExch(bad, 7);
-                conn16[cptr[t] + i] = (uint16_t)loc;
+                conn16[cptr[t] + (int)tpos[e0 + i / nref] * nref + i % nref] = (uint16_t)loc;
             }
         }
         __syncthreads();
     }
+}
+
+// Stage positions of a tile's elements (bank-conflict-aware order).  The reduce
+// warps load, per 16-lane half-warp, the first (second) contributions of 16 even
+// (odd) CSR slots of consecutive two-slot units; a load's 8-B stage word sits in
+// bank pair (sym * maxe + position) mod 16, and two lanes on the same bank pair
+// but different words serialise.  The compute warps write stage[sym][position]
+// for consecutive positions (conflict-free for ANY position order), so the order
+// is free: greedily, in ascending element id, each element takes the residue
+// class (position mod 16) that adds the fewest same-bank lanes to the load groups
+// it appears in (dense positions: class k holds ceil((ne - k) / 16) elements).
+// The summation order of every slot is unchanged (the slot words keep their
+// contributions in symbolic order), so the values are bitwise the same.
+constexpr int ORD_MAXM = 16384;     // light contributions per tile held in shared memory
+constexpr int ORD_MAXG = 2048;      // load groups per tile (4 per 32 slots)
+constexpr int ORD_MAXE = 4096;      // elements per tile
+constexpr size_t ORD_SMEM = sizeof(uint32_t) * (ORD_MAXM + ORD_MAXG * 4) + sizeof(int) * (2 * ORD_MAXE + 1) + ORD_MAXE;
+__global__ void __launch_bounds__(256)
+k_tile_order(int n_tiles, int nsym, int maxe, const int64_t* __restrict__ bounds, const int64_t* __restrict__ row_ptr,
+             const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ codes, const int64_t* __restrict__ ptr,
+             const int32_t* __restrict__ telems, uint16_t* __restrict__ tpos) {
+    extern __shared__ __align__(16) uint32_t ord_smem[];
+    uint32_t* mem = ord_smem;                   // (group << 6 | sym) of each light contribution, by element
+    uint32_t* gb = mem + ORD_MAXM;              // per group: 16 bank-pair counters (u8)
+    int* mptr = reinterpret_cast<int*>(gb + ORD_MAXG * 4);
+    int* mcur = mptr + ORD_MAXE + 1;
+    uint8_t* col = reinterpret_cast<uint8_t*>(mcur + ORD_MAXE);
+    __shared__ int fail;
+    const int tid = threadIdx.x, lane = tid & 31;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int64_t s0 = row_ptr[bounds[t]], s1 = row_ptr[bounds[t + 1]];
+        const int32_t* te = telems + ptr[t];
+        const int ne = (int)(ptr[t + 1] - ptr[t]);
+        const int64_t u0 = s0 >> 1;
+        const int ngr = (int)((((s1 + 1) >> 1) - u0 + 15) >> 4) * 4;
+        if (tid == 0) fail = (ne > ORD_MAXE || ngr > ORD_MAXG) ? 1 : 0;
+        for (int i = tid; i <= ne && i <= ORD_MAXE; i += 256) mptr[i] = 0;
+        for (int i = tid; i < ngr * 4 && i < ORD_MAXG * 4; i += 256) gb[i] = 0u;
+        __syncthreads();
+        // light contributions of the tile's slots -> (element, group, sym); counts first
+        for (int pass = 0; pass < 2 && !fail; ++pass) {
+            for (int64_t S = s0 + tid; S < s1; S += 256) {
+                const int j0 = slot_ptr[S], c = slot_ptr[S + 1] - j0;
+                if (c > 2) continue;
+                for (int ld = 0; ld < c; ++ld) {
+                    const int32_t cc = codes[j0 + ld];
+                    const int32_t le = cc / nsym;
+                    int lo = 0, hi = ne;
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (te[mid] < le) lo = mid + 1; else hi = mid;
+                    }
+                    if (lo >= ne) continue;
+                    if (pass == 0) {
+                        atomicAdd(&mptr[lo + 1], 1);
+                    } else {
+                        const int g = (int)((((S >> 1) - u0) >> 4) * 4 + (S & 1) * 2 + ld);
+                        const int k = atomicAdd(&mcur[lo], 1);
+                        if (k < ORD_MAXM) mem[k] = (uint32_t)g << 6 | (uint32_t)(cc - le * nsym);
+                    }
+                }
+            }
+            __syncthreads();
+            if (pass == 0) {
+                if (tid == 0) {  // exclusive scan of the counts (ne <= ORD_MAXE, once per tile)
+                    for (int i = 0; i < ne; ++i) mptr[i + 1] += mptr[i];
+                    if (mptr[ne] > ORD_MAXM) fail = 1;
+                }
+                __syncthreads();
+                for (int i = tid; i < ne; i += 256) mcur[i] = mptr[i];
+                __syncthreads();
+            }
+        }
+        if (!fail && tid < 32) {
+            // greedy residue classes, warp 0: lane k (< 16) prices class k, lanes 16..31 the
+            // second half of the element's contributions for class lane - 16
+            int used = 0;
+            const int k = lane & 15;
+            const int capk = k < ne ? (ne - k + 15) / 16 : 0;
+            for (int e = 0; e < ne; ++e) {
+                const int m0 = mptr[e], m1 = mptr[e + 1], mh = (m0 + m1) >> 1;
+                int cost = 0;
+                for (int m = (lane < 16 ? m0 : mh); m < (lane < 16 ? mh : m1); ++m) {
+                    const uint32_t w = mem[m];
+                    const int g = (int)(w >> 6), b = (int)(((w & 63u) * (uint32_t)maxe + (uint32_t)k) & 15u);
+                    cost += (int)((gb[g * 4 + (b >> 2)] >> (8 * (b & 3))) & 255u);
+                }
+                cost += __shfl_xor_sync(0xffffffffu, cost, 16);
+                // full classes are not candidates; ties -> the lowest class
+                int key = used < capk ? (cost << 5 | k) : 0x7fffffff;
+                for (int o = 8; o > 0; o >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, o));
+                const int best = key & 31;
+                if (k == best) ++used;
+                for (int m = m0 + lane; m < m1; m += 32) {
+                    const uint32_t w = mem[m];
+                    const int g = (int)(w >> 6), b = (int)(((w & 63u) * (uint32_t)maxe + (uint32_t)best) & 15u);
+                    atomicAdd(&gb[g * 4 + (b >> 2)], 1u << (8 * (b & 3)));
+                }
+                if (lane == 0) col[e] = (uint8_t)best;
+                __syncwarp();
+            }
+            // dense positions: class c, in ascending element order, takes c, c + 16, c + 32, ...
+            if (lane < 16) {
+                int r = 0;
+                for (int e = 0; e < ne; ++e)
+                    if (col[e] == lane) tpos[ptr[t] + e] = (uint16_t)(lane + 16 * r++);
+            }
+        }
+        if (fail)
+            for (int e = tid; e < ne; e += 256) tpos[ptr[t] + e] = (uint16_t)e;  // identity order
+        __syncthreads();
+    }
+}
+
+// the tile's elements in stage-position order (the kernel reports degenerate elements through it)
+__global__ void k_tile_scatter(int n_tiles, const int64_t* __restrict__ ptr, const int32_t* __restrict__ telems,
+                               const uint16_t* __restrict__ tpos, int32_t* __restrict__ out) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x)
+        for (int64_t i = ptr[t]; i < ptr[t + 1]; ++i) out[ptr[t] + tpos[i]] = telems[i];
 }
 
 // per-tile scalars {s0, ns, e0, ne}, {q0, nq, h0, nh}, {g0, nrows, l0, nl} (all < 2^31) and maxima
@@ -460,13 +580,26 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
         scope.drop(tile_of);
         return LFEM_OK;
     }
+    // bank-conflict-aware stage positions of every tile's elements (k_tile_order)
+    uint16_t* tpos = nullptr;
+    scope.track(&tpos);
+    LFEM_TRY(dev_alloc_t(&tpos, total + 8, s));
+    {
+        LFEM_TRY(ensure_smem_attr(reinterpret_cast<const void*>(k_tile_order), (int)ORD_SMEM));
+        k_tile_order<<<n_tiles < 148 * 4 ? n_tiles : 148 * 4, 256, ORD_SMEM, s>>>(
+            n_tiles, p->mesh->nsym, maxe, bounds, p->row_ptr, p->slot_ptr, p->codes, ptr, T.tile_elems, tpos);
+        LFEM_CUDA(cudaGetLastError());
+    }
+    LFEM_TRY(dev_alloc_t(&T.tile_elems_pos, total + 1, s));
+    k_tile_scatter<<<grid_for(n_tiles, 128), 128, 0, s>>>(n_tiles, ptr, T.tile_elems, tpos, T.tile_elems_pos);
+    LFEM_CUDA(cudaGetLastError());
     // halo nodes per tile (pass 0: counts)
     int32_t* hcnt = nullptr;
     scope.track(&hcnt);
     LFEM_TRY(dev_alloc_t(&hcnt, n_tiles + 1, s));
     const unsigned node_grid = n_tiles < 148 * 8 ? n_tiles : 148 * 8;
     k_tile_nodes<0><<<node_grid, 256, 0, s>>>(n_tiles, nref, p->row_begin, bounds, ptr, T.tile_elems, p->local_conn,
-                                              hcnt, nullptr, nullptr, nullptr, nullptr, flags);
+                                              hcnt, nullptr, nullptr, nullptr, nullptr, nullptr, flags);
     LFEM_CUDA(cudaGetLastError());
     // element / connectivity / halo offsets as int32 (host; n_tiles is small)
     int32_t* eptr32 = nullptr;
@@ -501,7 +634,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
         LFEM_CUDA(cudaMemcpy(cptr32, cp.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
         LFEM_CUDA(cudaMemcpy(lptr32, lp.data(), sizeof(int32_t) * (n_tiles + 1), cudaMemcpyHostToDevice));
         k_tile_nodes<1><<<node_grid, 256, 0, s>>>(n_tiles, nref, p->row_begin, bounds, ptr, T.tile_elems,
-                                                  p->local_conn, hcnt, lptr32, cptr32, T.halo, T.conn16, flags);
+                                                  p->local_conn, hcnt, lptr32, cptr32, T.halo, T.conn16, tpos, flags);
         LFEM_CUDA(cudaGetLastError());
         int hb = 0;
         LFEM_CUDA(cudaMemcpyAsync(&hb, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -535,7 +668,8 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     if (n_rows > 0) {
         k_tile_pairs<<<grid_for(n_rows, 128), 128, 0, s>>>(n_rows, tile_of, bounds, hw, p->mesh->nsym, maxe, p->row_ptr,
                                                            p->slot_ptr,
-                                                           p->codes, ptr, T.tile_elems, hptr, T.pairs, T.heavy, flags);
+                                                           p->codes, ptr, T.tile_elems, tpos, hptr, T.pairs, T.heavy,
+                                                           flags);
         LFEM_CUDA(cudaGetLastError());
     }
     LFEM_TRY(dev_alloc_t(&T.tile_info, (size_t)3 * n_tiles + 3, s));
@@ -556,6 +690,7 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     scope.drop(hcnt);
     scope.drop(bounds);
     scope.drop(tile_of);
+    scope.drop(tpos);
     if (h[0]) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tile code construction failed (" + std::to_string(h[0]) + ")");
     T.max_tile_slots = h[2];
     T.max_tile_heavy = h[3];
