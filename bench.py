@@ -364,19 +364,6 @@ def run_rhs(args):
     prof = lfem.lfem_profile_read(plan)
     lfem.lfem_profile_enable(plan, False)
     clk = clocks.stop()
-    # per-rank shape of the partition (N > 1): rows, nnz, elements assembled (halo included), device ms
-    mine_info = torch.tensor([plan.n_rows, plan.nnz, plan.n_elems_local, elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        parts = [torch.empty_like(mine_info) for _ in range(world)]
-        dist.all_gather(parts, mine_info)
-        info = torch.stack(parts).cpu().numpy()
-    else:
-        info = mine_info.cpu().numpy()[None, :]
-    ranks = {"rows": [int(v) for v in info[:, 0]], "nnz": [int(v) for v in info[:, 1]],
-             "n_elems_local": [int(v) for v in info[:, 2]],
-             "ms_per_step": [float(v) / args.steps for v in info[:, 3]],
-             "nnz_spread_max_over_min": float(info[:, 1].max() / max(1.0, info[:, 1].min())),
-             "halo_factor_per_rank": [float(v) * world / n_elems for v in info[:, 2]]}
     tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
@@ -532,19 +519,6 @@ def run_mcf(args):
     torch.cuda.synchronize()
     prof_step_ms = t0p.elapsed_time(t1p) / nprof
     clk = clocks.stop()
-    # per-rank shape of the partition (N > 1): rows, nnz, elements assembled (halo included), device ms
-    mine_info = torch.tensor([plan.n_rows, plan.nnz, plan.n_elems_local, elapsed_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        parts = [torch.empty_like(mine_info) for _ in range(world)]
-        dist.all_gather(parts, mine_info)
-        info = torch.stack(parts).cpu().numpy()
-    else:
-        info = mine_info.cpu().numpy()[None, :]
-    ranks = {"rows": [int(v) for v in info[:, 0]], "nnz": [int(v) for v in info[:, 1]],
-             "n_elems_local": [int(v) for v in info[:, 2]],
-             "ms_per_step": [float(v) / args.steps for v in info[:, 3]],
-             "nnz_spread_max_over_min": float(info[:, 1].max() / max(1.0, info[:, 1].min())),
-             "halo_factor_per_rank": [float(v) * world / n_elems for v in info[:, 2]]}
     tmax = torch.tensor([elapsed_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)

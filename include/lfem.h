@@ -105,7 +105,12 @@ typedef enum {
     LFEM_QUAD_TRI16_DEG8 = 5, /* Dunavant 16-point degree-8 rule, P2 triangles only (the paper's
                                  load-vector rule) */
     LFEM_QUAD_LINE2_DEG3 = 6, /* 2-point Gauss-Legendre (P1 curves) */
-    LFEM_QUAD_LINE3_DEG5 = 7  /* 3-point Gauss-Legendre (P2 curves) */
+    LFEM_QUAD_LINE3_DEG5 = 7, /* 3-point Gauss-Legendre (P2 curves) */
+    LFEM_QUAD_TET35_DEG7 = 8, /* 35-point fully symmetric positive degree-7 rule, P2 tets only (the
+                                 paper's Jaskowiec-Sukumar degree-7 rule; constants derived
+                                 from the moment equations, reading G39) */
+    LFEM_QUAD_LINE6_DEG11 = 9 /* 6-point Gauss-Legendre, P2 curves only (the paper's order-10 Gauss
+                                 rule for curves, reading G38) */
 } lfem_quad;
 
 /* 'kinds' bitmask of lfem_assemble_numeric; vals[] index = bit position. */

@@ -122,6 +122,8 @@ QUAD_TET11_DEG4 = 4
 QUAD_TRI16_DEG8 = 5  # Dunavant degree 8 (the paper's load-vector rule)
 QUAD_LINE2_DEG3 = 6  # 2-point Gauss-Legendre (curves)
 QUAD_LINE3_DEG5 = 7  # 3-point Gauss-Legendre
+QUAD_TET35_DEG7 = 8  # 35-point symmetric degree-7 tet rule (stands in for Jaskowiec-Sukumar degree 7)
+QUAD_LINE6_DEG11 = 9  # 6-point Gauss-Legendre (the paper's order-10 Gauss rule for curves)
 SURFACE_LINE = 2     # curves in R^3 (Table 4 "surface 1D")
 
 

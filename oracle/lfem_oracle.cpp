@@ -68,7 +68,7 @@ namespace {
 
 enum { SURFACE_TRI = 0, BULK_TET = 1, SURFACE_LINE = 2 };
 enum { Q_DEFAULT = 0, Q_TRI3_DEG2 = 1, Q_TRI6_DEG4 = 2, Q_TET4_DEG2 = 3, Q_TET11_DEG4 = 4, Q_TRI16_DEG8 = 5,
-       Q_LINE2_DEG3 = 6, Q_LINE3_DEG5 = 7 };
+       Q_LINE2_DEG3 = 6, Q_LINE3_DEG5 = 7, Q_TET35_DEG7 = 8, Q_LINE6_DEG11 = 9 };
 
 // dimension of the reference element: curves 1, surfaces 2, bulk 3
 int dim_of(int domain) { return domain == SURFACE_LINE ? 1 : domain == SURFACE_TRI ? 2 : 3; }
@@ -163,6 +163,50 @@ bool make_rule(int quad, std::vector<QPoint>& r) {
         }
         return true;
     }
+    case Q_LINE6_DEG11: {
+        // 6-point Gauss-Legendre on [0, 1] (reading G38: the paper's "Gauss ... of order 10" for
+        // curves, read as the smallest Gauss rule exact to degree >= 10, i.e. degree 11):
+        // nodes are the roots of P_6 mapped to [0, 1], weights w = 1 / ((1 - t^2) P_6'(t)^2)
+        // (halved for the unit interval) -- computed here by Newton on the three-term recurrence
+        for (int k = 0; k < 6; ++k) {
+            double t = std::cos(M_PI * (k + 0.75) / 6.5), dp = 0.0;
+            for (int it = 0; it < 100; ++it) {
+                double p0 = 1.0, p1 = t;
+                for (int n = 2; n <= 6; ++n) {
+                    const double p2 = ((2.0 * n - 1.0) * t * p1 - (n - 1.0) * p0) / n;
+                    p0 = p1;
+                    p1 = p2;
+                }
+                dp = 6.0 * (t * p1 - p0) / (t * t - 1.0);
+                const double dt = p1 / dp;
+                t -= dt;
+                if (std::fabs(dt) < 1e-17) break;
+            }
+            QPoint q;
+            q.lam[1] = 0.5 * (1.0 + t);
+            q.lam[0] = 1.0 - q.lam[1];
+            q.lam[2] = q.lam[3] = 0.0;
+            q.w = 1.0 / ((1.0 - t * t) * dp * dp);  // (2 / ((1 - t^2) P6'^2)) / 2
+            r.push_back(q);
+        }
+        return true;
+    }
+    case Q_TET35_DEG7: {
+        // fully symmetric, positive, interior degree-7 rule with 35 points (reading G39: stands in
+        // for the paper's Jaskowiec-Sukumar degree-7 tetrahedral rule, whose constants are not
+        // in the container): orbits S4, S31 (a), S22 (a), 2 x S211 (a, b); solved here from the
+        // degree-7 moment equations of the S4-invariant polynomials (50 digits), weights for volume 1/6
+        add_orbit4(r, 0.25, 0.25, 0.25, 0.25, 0.01591421491068847481009640601953773030655);
+        const double a1 = 0.315701149778202799423429999593311488426;
+        add_orbit4(r, a1, a1, a1, 1.0 - 3.0 * a1, 0.00705493020166117151271436179975778958127);
+        const double a2 = 0.4495101774016036312369461770134375340242;
+        add_orbit4(r, a2, a2, 0.5 - a2, 0.5 - a2, 0.005316154638809596655712470680490409516245);
+        const double a3 = 0.1888338310260010477364311038545857550051, b3 = 0.5751716375870000234832415770223075196671;
+        add_orbit4(r, a3, a3, b3, 1.0 - 2.0 * a3 - b3, 0.006201188454722436894935926865246853385281);
+        const double a4 = 0.02126547254148324598883610149981994107435, b4 = 0.1466388138184849469042224171521277240548;
+        add_orbit4(r, a4, a4, b4, 1.0 - 2.0 * a4 - b4, 0.001351795138317223594350572248516090026183);
+        return true;
+    }
     case Q_TET4_DEG2: {
         const double s5 = std::sqrt(5.0);
         const double al = (5.0 - s5) / 20.0, be = (5.0 + 3.0 * s5) / 20.0;
@@ -253,8 +297,8 @@ bool make_ref(int domain, int order, int quad, Ref& R) {
         else quad = (order == 1) ? Q_TET4_DEG2 : Q_TET11_DEG4;
     }
     if (domain == SURFACE_TRI && quad != Q_TRI3_DEG2 && quad != Q_TRI6_DEG4 && quad != Q_TRI16_DEG8) return false;
-    if (domain == BULK_TET && quad != Q_TET4_DEG2 && quad != Q_TET11_DEG4) return false;
-    if (domain == SURFACE_LINE && quad != Q_LINE2_DEG3 && quad != Q_LINE3_DEG5) return false;
+    if (domain == BULK_TET && quad != Q_TET4_DEG2 && quad != Q_TET11_DEG4 && quad != Q_TET35_DEG7) return false;
+    if (domain == SURFACE_LINE && quad != Q_LINE2_DEG3 && quad != Q_LINE3_DEG5 && quad != Q_LINE6_DEG11) return false;
     R.domain = domain;
     R.order = order;
     R.d = dim_of(domain);
@@ -495,9 +539,9 @@ void oracle_free(oracle_csr* c) {
 int oracle_nref(int domain, int order) { return nref_of(domain, order); }
 
 // Quadrature rule as used by the oracle (for the exactness pins).
-int oracle_rule(int quad, int* nq, double* lam /* 16 x 4 */, double* w /* 16 */) {
+int oracle_rule(int quad, int* nq, double* lam /* 64 x 4 */, double* w /* 64 */) {
     std::vector<QPoint> r;
-    if (!make_rule(quad, r)) return ERR_UNSUPPORTED;
+    if (!make_rule(quad, r) || r.size() > 64) return ERR_UNSUPPORTED;
     *nq = (int)r.size();
     for (size_t q = 0; q < r.size(); ++q) {
         for (int i = 0; i < 4; ++i) lam[4 * q + i] = r[q].lam[i];

@@ -188,8 +188,8 @@ def assemble_rhs_rows(mesh, u, kind="load", rows=None, nthreads: Optional[int] =
 def rule(quad: int):
     """(lam (nq,4), w (nq,)) of the oracle's quadrature rule."""
     L = lib()
-    lam = np.zeros((16, 4))
-    w = np.zeros(16)
+    lam = np.zeros((64, 4))
+    w = np.zeros(64)
     nq = ctypes.c_int(0)
     st = L.oracle_rule(quad, ctypes.byref(nq), _p(lam), _p(w))
     if st != 0:

@@ -239,8 +239,9 @@ lfem_status lfem_mesh_create(lfem_domain dom, int order, lfem_quad quad, int64_t
     }
     // each family runs with the rule its constant tables were built for
     const int fam = family_of(dom, order, q);
-    const int want[7] = {LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4,  LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4,
-                         LFEM_QUAD_TRI16_DEG8, LFEM_QUAD_LINE2_DEG3, LFEM_QUAD_LINE3_DEG5};
+    const int want[N_FAMILIES] = {LFEM_QUAD_TRI3_DEG2,  LFEM_QUAD_TRI6_DEG4,  LFEM_QUAD_TET4_DEG2,
+                                  LFEM_QUAD_TET11_DEG4, LFEM_QUAD_TRI16_DEG8, LFEM_QUAD_LINE2_DEG3,
+                                  LFEM_QUAD_LINE3_DEG5, LFEM_QUAD_TET35_DEG7, LFEM_QUAD_LINE6_DEG11};
     if (q != want[fam])
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "quadrature rule not available for this (domain, order)");
     if (n_nodes < 0 || n_elems < 0 || n_nodes >= INT_MAX || n_elems >= INT_MAX)
@@ -249,9 +250,9 @@ lfem_status lfem_mesh_create(lfem_domain dom, int order, lfem_quad quad, int64_t
         return lfem_fail(LFEM_ERR_INVALID_ARG, "coords / conn is NULL");
     if ((reinterpret_cast<uintptr_t>(coords) & 7) || (reinterpret_cast<uintptr_t>(conn) & 3))
         return lfem_fail(LFEM_ERR_INVALID_ARG, "coords must be 8-byte and conn 4-byte aligned");
-    static const int nrefs[7] = {3, 6, 4, 10, 6, 2, 3};
-    static const int nqs[7] = {3, 6, 4, 11, 16, 2, 3};
-    static const int nsyms[7] = {6, 21, 10, 55, 21, 3, 6};
+    static const int nrefs[N_FAMILIES] = {3, 6, 4, 10, 6, 2, 3, 10, 3};
+    static const int nqs[N_FAMILIES] = {3, 6, 4, 11, 16, 2, 3, 35, 6};
+    static const int nsyms[N_FAMILIES] = {6, 21, 10, 55, 21, 3, 6, 55, 6};
     lfem_mesh_s* m = new (std::nothrow) lfem_mesh_s();
     if (!m) return lfem_fail(LFEM_ERR_NOMEM, "host allocation");
     m->domain = dom;

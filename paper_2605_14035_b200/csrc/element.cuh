@@ -112,6 +112,8 @@ template <> struct FamShape<FAM_TRI_P2> { using S = Shape<2, 2>; };
 template <> struct FamShape<FAM_TRI_P2_Q16> { using S = Shape<2, 2>; };
 template <> struct FamShape<FAM_LINE_P1> { using S = Shape<1, 1>; };
 template <> struct FamShape<FAM_LINE_P2> { using S = Shape<1, 2>; };
+template <> struct FamShape<FAM_LINE_P2_Q6> { using S = Shape<1, 2>; };
+template <> struct FamShape<FAM_TET_P2_Q35> { using S = Shape<3, 2>; };
 template <> struct FamShape<FAM_TET_P1> { using S = Shape<3, 1>; };
 template <> struct FamShape<FAM_TET_P2> { using S = Shape<3, 2>; };
 
@@ -143,16 +145,19 @@ __device__ __forceinline__ double rcp_nr(double x) {
 }
 
 // reference coordinates of the quadrature points (constant memory)
+constexpr int MAX_NQ = 35;
 struct QuadXi {
-    double xi[16][3];
+    double xi[MAX_NQ][3];
 };
-__constant__ QuadXi c_xi[7];
+__constant__ QuadXi c_xi[N_FAMILIES];
 
 enum Kind { KIND_M = 0, KIND_A = 1, KIND_AA = 2 };
 
 template <int F>
 struct Elem {
     static constexpr int N = FamInfo<F>::NREF, D = FamInfo<F>::D, NQ = FamInfo<F>::NQ, NS = FamInfo<F>::NSYM;
+    // quadrature loops are unrolled except for the 35-point tet rule (code size / compile time)
+    static constexpr int QU = (D == 3 && NQ > 16) ? 1 : NQ;
     using S = typename FamShape<F>::S;
     static_assert(S::N == N, "shape table");
 
@@ -271,7 +276,7 @@ struct Elem {
 #pragma unroll
                         for (int al = 0; al < 6; ++al) g.mom[m][c][al] = 0.0;
             }
-#pragma unroll
+#pragma unroll QU
             for (int q = 0; q < NQ; ++q) {
                 double J[3][D];
                 jac_at(J0, J1, q, J);
@@ -352,7 +357,7 @@ struct Elem {
         double m[NS];
 #pragma unroll
         for (int s = 0; s < NS; ++s) m[s] = 0.0;
-#pragma unroll
+#pragma unroll QU
         for (int q = 0; q < NQ; ++q) {
             const double wmu = P1S ? T.w[q] * g.mu1 : g.wmu[q];
 #pragma unroll
@@ -432,7 +437,7 @@ struct Elem {
             double acc[NS];
 #pragma unroll
             for (int s = 0; s < NS; ++s) acc[s] = 0.0;
-#pragma unroll
+#pragma unroll QU
             for (int q = 0; q < NQ; ++q) {
                 double J[3][D], C[3][3];
                 jac_at(g.J0, g.J1, q, J);

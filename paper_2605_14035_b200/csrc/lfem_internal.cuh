@@ -13,7 +13,8 @@
 // element families
 // ---------------------------------------------------------------------------
 enum Family { FAM_TRI_P1 = 0, FAM_TRI_P2 = 1, FAM_TET_P1 = 2, FAM_TET_P2 = 3, FAM_TRI_P2_Q16 = 4, FAM_LINE_P1 = 5,
-              FAM_LINE_P2 = 6 };
+              FAM_LINE_P2 = 6, FAM_TET_P2_Q35 = 7, FAM_LINE_P2_Q6 = 8 };
+constexpr int N_FAMILIES = 9;
 
 template <int F> struct FamInfo;
 template <> struct FamInfo<FAM_TRI_P1> { static constexpr int NREF = 3, D = 2, NQ = 3, NSYM = 6; };
@@ -25,6 +26,10 @@ template <> struct FamInfo<FAM_TRI_P2_Q16> { static constexpr int NREF = 6, D = 
 // curves: Gauss-Legendre 2 / 3 points
 template <> struct FamInfo<FAM_LINE_P1> { static constexpr int NREF = 2, D = 1, NQ = 2, NSYM = 3; };
 template <> struct FamInfo<FAM_LINE_P2> { static constexpr int NREF = 3, D = 1, NQ = 3, NSYM = 6; };
+// the paper's other rules: a 35-point degree-7 tet rule (reading G39)
+// and the 6-point Gauss-Legendre rule (order 10 for curves, reading G38)
+template <> struct FamInfo<FAM_TET_P2_Q35> { static constexpr int NREF = 10, D = 3, NQ = 35, NSYM = 55; };
+template <> struct FamInfo<FAM_LINE_P2_Q6> { static constexpr int NREF = 3, D = 1, NQ = 6, NSYM = 6; };
 
 // index of (a, b), a <= b, in the row-major upper triangle of an n x n matrix
 __host__ __device__ constexpr int sym_index(int n, int a, int b) {
@@ -199,7 +204,9 @@ lfem_status check_conn_launch(const int32_t* conn, int64_t n_elems, int nref, in
                               cudaStream_t s);
 
 inline int family_of(int domain, int order, int quad = LFEM_QUAD_DEFAULT) {
-    if (domain == LFEM_SURFACE_LINE) return order == 1 ? FAM_LINE_P1 : FAM_LINE_P2;
+    if (domain == LFEM_SURFACE_LINE)
+        return order == 1 ? FAM_LINE_P1 : quad == LFEM_QUAD_LINE6_DEG11 ? FAM_LINE_P2_Q6 : FAM_LINE_P2;
+    if (domain == LFEM_BULK_TET && order == 2 && quad == LFEM_QUAD_TET35_DEG7) return FAM_TET_P2_Q35;
     if (domain == LFEM_SURFACE_TRI && order == 2 && quad == LFEM_QUAD_TRI16_DEG8) return FAM_TRI_P2_Q16;
     if (domain == LFEM_SURFACE_TRI) return order == 1 ? FAM_TRI_P1 : FAM_TRI_P2;
     return order == 1 ? FAM_TET_P1 : FAM_TET_P2;

@@ -35,6 +35,7 @@ namespace {
 
 template <int F> struct V0Cfg { static constexpr int MINB = 1; };
 template <> struct V0Cfg<FAM_TET_P2> { static constexpr int MINB = LFEM_V0_TET_MINB; };
+template <> struct V0Cfg<FAM_TET_P2_Q35> { static constexpr int MINB = 1; };
 
 // --------------------------------------------------------------------------
 // V0: element kernel -> stage[k][s][le]; slot kernel -> vals
@@ -274,6 +275,8 @@ lfem_status upload_reference_tables() {
     static RefTab<FAM_TRI_P2_Q16> t5;
     static RefTab<FAM_LINE_P1> t6;
     static RefTab<FAM_LINE_P2> t7;
+    static RefTab<FAM_TET_P2_Q35> t8;
+    static RefTab<FAM_LINE_P2_Q6> t9;
     refhost::fill(t1, refhost::rule_tri3(), 2, 1);
     refhost::fill(t2, refhost::rule_tri6(), 2, 2);
     refhost::fill(t3, refhost::rule_tet4(), 3, 1);
@@ -281,6 +284,8 @@ lfem_status upload_reference_tables() {
     refhost::fill(t5, refhost::rule_tri16(), 2, 2);
     refhost::fill(t6, refhost::rule_line(2), 1, 1);
     refhost::fill(t7, refhost::rule_line(3), 1, 2);
+    refhost::fill(t8, refhost::rule_tet35(), 3, 2);
+    refhost::fill(t9, refhost::rule_line(6), 1, 2);
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri1, &t1, sizeof(t1)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri2, &t2, sizeof(t2)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tet1, &t3, sizeof(t3)));
@@ -288,11 +293,13 @@ lfem_status upload_reference_tables() {
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tri2q, &t5, sizeof(t5)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_line1, &t6, sizeof(t6)));
     LFEM_CUDA(cudaMemcpyToSymbol(c_tab_line2, &t7, sizeof(t7)));
-    QuadXi xi[7] = {};
-    const refhost::Rule rules[7] = {refhost::rule_tri3(),  refhost::rule_tri6(),   refhost::rule_tet4(),
-                                    refhost::rule_tet11(), refhost::rule_tri16(),  refhost::rule_line(2),
-                                    refhost::rule_line(3)};
-    for (int f = 0; f < 7; ++f)
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_tet2q, &t8, sizeof(t8)));
+    LFEM_CUDA(cudaMemcpyToSymbol(c_tab_line2q, &t9, sizeof(t9)));
+    static QuadXi xi[N_FAMILIES] = {};
+    static const refhost::Rule rules[N_FAMILIES] = {refhost::rule_tri3(),  refhost::rule_tri6(),   refhost::rule_tet4(),
+                                                    refhost::rule_tet11(), refhost::rule_tri16(),  refhost::rule_line(2),
+                                                    refhost::rule_line(3), refhost::rule_tet35(), refhost::rule_line(6)};
+    for (int f = 0; f < N_FAMILIES; ++f)
         for (int q = 0; q < rules[f].nq; ++q)
             for (int m = 0; m < 3; ++m) xi[f].xi[q][m] = rules[f].xi[q][m];
     LFEM_CUDA(cudaMemcpyToSymbol(c_xi, xi, sizeof(xi)));
@@ -348,6 +355,8 @@ lfem_status numeric_dispatch(lfem_plan_s* p, unsigned kinds, const double* coord
     case FAM_TRI_P2_Q16: return dispatch_kinds<FAM_TRI_P2_Q16>(p, kinds, coords, coeff, vals, s);
     case FAM_LINE_P1: return dispatch_kinds<FAM_LINE_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_LINE_P2: return dispatch_kinds<FAM_LINE_P2>(p, kinds, coords, coeff, vals, s);
+    case FAM_LINE_P2_Q6: return dispatch_kinds<FAM_LINE_P2_Q6>(p, kinds, coords, coeff, vals, s);
+    case FAM_TET_P2_Q35: return dispatch_kinds<FAM_TET_P2_Q35>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P1: return dispatch_kinds<FAM_TET_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TET_P2: return dispatch_kinds<FAM_TET_P2>(p, kinds, coords, coeff, vals, s);
     }

@@ -57,6 +57,9 @@
 #ifndef LFEM_REGS_R
 #define LFEM_REGS_R 88
 #endif
+#ifndef LFEM_NMB  // tile metadata buffers (tiles in flight ahead of the compute warps)
+#define LFEM_NMB 3
+#endif
 #ifndef LFEM_NSB  // stage buffers (kind passes in flight between compute and reduce warps)
 #define LFEM_NSB 2
 #endif
@@ -125,10 +128,11 @@ template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, R
 template <> struct TileCfg<FAM_TRI_P2_Q16> : TileCfg<FAM_TRI_P2> {};
 template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, REGS_C = 0, REGS_R = 0; };
 template <> struct TileCfg<FAM_TET_P2> { static constexpr int CW = 4, RW = 4, MINB = 1, EPT = 1, REGS_C = 0, REGS_R = 0; };
+template <> struct TileCfg<FAM_TET_P2_Q35> : TileCfg<FAM_TET_P2> {};
 
 struct TileLayout {
     size_t stage_bytes;           // one stage buffer
-    size_t meta_off[3], conn_off, pairs_off, heavy_off, halo_off, meta_bytes;
+    size_t meta_off[LFEM_NMB], conn_off, pairs_off, heavy_off, halo_off, meta_bytes;
     size_t node_off[2], xyz_off, u_off, node_bytes, total;
 };
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -146,8 +150,8 @@ __host__ __device__ inline TileLayout tile_layout(int nsym, int nref, int maxe, 
     L.u_off = align16(sizeof(double) * (3 * (size_t)nodes_cap + 2));
     L.node_bytes = L.u_off + align16(sizeof(double) * ((size_t)nodes_cap + 2));
     size_t o = LFEM_NSB * L.stage_bytes;
-    for (int b = 0; b < 3; ++b) L.meta_off[b] = o + b * L.meta_bytes;
-    o += 3 * L.meta_bytes;
+    for (int b = 0; b < LFEM_NMB; ++b) L.meta_off[b] = o + b * L.meta_bytes;
+    o += LFEM_NMB * L.meta_bytes;
     for (int b = 0; b < 2; ++b) L.node_off[b] = o + b * L.node_bytes;
     L.total = o + 2 * L.node_bytes;
     return L;
@@ -181,7 +185,7 @@ struct StageSink {  // stage[s * maxe + e]
 
 // producer: publish tile t's info in sinfo[b] and start its bulk copies into meta buffer b
 __device__ __forceinline__ void issue_tile(const TileArgs& a, unsigned char* smem, const TileLayout& lay, int t,
-                                           int b, int4 (*sinfo)[3], uint64_t* bar) {
+                                           int b, int4 (*sinfo)[3], uint64_t* bar) {  // sinfo[LFEM_NMB][3]
     const int4 i0 = a.tile_info[3 * t], i1 = a.tile_info[3 * t + 1], i2 = a.tile_info[3 * t + 2];
     sinfo[b][0] = i0;
     sinfo[b][1] = i1;
@@ -281,10 +285,10 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
     using Cfg = TileCfg<F>;
     constexpr int N = E::N, CW = Cfg::CW, RW = Cfg::RW, EPT = Cfg::EPT, CT = CW * 32;
     unsigned char* smem = reinterpret_cast<unsigned char*>(tile_smem_d);
-    __shared__ int meta_done[3];  // reduce warps done with the tile in meta buffer b
-    __shared__ __align__(8) uint64_t meta_full[3], stage_full[LFEM_NSB], stage_empty[LFEM_NSB], node_full[2],
+    __shared__ int meta_done[LFEM_NMB];  // reduce warps done with the tile in meta buffer b
+    __shared__ __align__(8) uint64_t meta_full[LFEM_NMB], stage_full[LFEM_NSB], stage_empty[LFEM_NSB], node_full[2],
         node_empty[2];
-    __shared__ int4 sinfo[3][3];
+    __shared__ int4 sinfo[LFEM_NMB][3];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
     const size_t node0 = lay.node_off[0], node_stride = lay.node_off[1] - lay.node_off[0];
 
     if (tid == 0) {
-        for (int b = 0; b < 3; ++b) {
+        for (int b = 0; b < LFEM_NMB; ++b) {
             mbar_init(&meta_full[b], 1);
             meta_done[b] = 0;
         }
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
     }
     __syncthreads();
     if (tid == CT) {
-        for (int k = 0; k < 3; ++k) {
+        for (int k = 0; k < LFEM_NMB; ++k) {
             const int t = blockIdx.x + k * G;
             if (t < a.n_tiles) issue_tile(a, smem, lay, t, k, sinfo, meta_full);
         }
@@ -328,7 +332,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
         prefetch_tile_nodes(a, DAA, sinfo[0][2], reinterpret_cast<const int32_t*>(smem + meta0 + lay.halo_off),
                             smem + node0, lay, &node_full[0], tid, CT);
         for (int it = 0; t < a.n_tiles; ++it, t += G) {
-            const int b = it % 3, nb = it & 1;
+            const int b = it % LFEM_NMB, nb = it & 1;
             const int4 i0 = sinfo[b][0], i2 = sinfo[b][2];
             const int e0 = i0.z, ne = i0.w;
             // this tile's node buffer: bulk copies + every thread's halo gathers, one mbarrier
@@ -344,8 +348,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                     atomicMin(a.err, __ldg(&a.elem_list[__ldg(&a.tile_elems[e0 + e])]));
             }
             if (t + G < a.n_tiles) {  // next tile's nodes -> the other node buffer, in flight during the kinds
-                const int bn = (it + 1) % 3;
-                mbar_wait(&meta_full[bn], ((it + 1) / 3) & 1);
+                const int bn = (it + 1) % LFEM_NMB;
+                mbar_wait(&meta_full[bn], ((it + 1) / LFEM_NMB) & 1);
                 const int fill = (it + 1) >> 1;  // fill index of buffer nb ^ 1: its previous contents must be read
                 if (fill > 0) mbar_wait(&node_empty[nb ^ 1], (fill - 1) & 1);
                 prefetch_tile_nodes(a, DAA, sinfo[bn][2],
@@ -389,8 +393,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
         (void)rw;
         uint32_t pass = 0;
         for (int it = 0, t = blockIdx.x; t < a.n_tiles; ++it, t += G) {
-            const int b = it % 3;
-            mbar_wait(&meta_full[b], (it / 3) & 1);
+            const int b = it % LFEM_NMB;
+            mbar_wait(&meta_full[b], (it / LFEM_NMB) & 1);
             const int4 i0 = sinfo[b][0], i1 = sinfo[b][1];
             const int s0 = i0.x, ns = (LFEM_TILED_SKIP & 2) ? 0 : i0.y, se = s0 + ns;
             const unsigned char* mb = smem + meta0 + b * meta_stride;
@@ -466,7 +470,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 if (done == RW - 1) {
                     meta_done[b] = 0;
                     __threadfence_block();
-                    if (t + 3 * G < a.n_tiles) issue_tile(a, smem, lay, t + 3 * G, b, sinfo, meta_full);
+                    if (t + LFEM_NMB * G < a.n_tiles) issue_tile(a, smem, lay, t + LFEM_NMB * G, b, sinfo, meta_full);
                 }
             }
         }
@@ -595,8 +599,10 @@ inline int tiled_default_variant(lfem_plan_s* p) {
 
 inline lfem_status tiled_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, const double* coeff,
                                   double* const vals[3], cudaStream_t s) {
-    if (p->mesh->family == FAM_LINE_P1 || p->mesh->family == FAM_LINE_P2)
+    if (p->mesh->family == FAM_LINE_P1 || p->mesh->family == FAM_LINE_P2 || p->mesh->family == FAM_LINE_P2_Q6)
         return lfem_fail(LFEM_ERR_UNSUPPORTED, "the tiled variant has no curve configuration (use V0 / AUTO)");
+    if (p->mesh->family == FAM_TET_P2_Q35)
+        return lfem_fail(LFEM_ERR_UNSUPPORTED, "the tiled variant has no 35-point tet configuration (use V0 / AUTO)");
     switch (p->mesh->family) {
     case FAM_TRI_P1: return tiled_kinds<FAM_TRI_P1>(p, kinds, coords, coeff, vals, s);
     case FAM_TRI_P2: return tiled_kinds<FAM_TRI_P2>(p, kinds, coords, coeff, vals, s);

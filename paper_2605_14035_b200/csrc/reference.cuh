@@ -16,6 +16,7 @@
 //                   grad_a . C C^T grad_b = d_a^T G^{-1} d_b)
 //   mono[q][0..5] = 1, x, y, x^2, xy, y^2 at xi_q = (x, y) (surface stiffness moments)
 #pragma once
+#include <algorithm>
 #include <cmath>
 
 #include "lfem_internal.cuh"
@@ -24,12 +25,13 @@ template <int F>
 struct RefTab {
     static constexpr int NREF = FamInfo<F>::NREF, D = FamInfo<F>::D, NQ = FamInfo<F>::NQ,
                          NSYM = FamInfo<F>::NSYM;
+    // (tables a family's kernels never read are one entry long: 64 KB of constant memory)
     double w[NQ];
     double phi[NQ][NREF];
-    double dphi[NQ][NREF][D];
+    double dphi[D == 3 ? NQ : 1][NREF][D];   // bulk stiffness (gradient form)
     double pp[NQ][NSYM];
-    double gg[NQ][NSYM][3];
-    double mono[NQ][6];  // 1, x, y, x^2, x y, y^2 at xi_q (surface stiffness moments)
+    double gg[D == 1 ? NQ : 1][NSYM][3];     // curves (metric form)
+    double mono[D == 2 ? NQ : 1][6];         // surfaces: 1, x, y, x^2, x y, y^2 at xi_q (stiffness moments)
 };
 
 __constant__ RefTab<FAM_TRI_P1> c_tab_tri1;
@@ -39,6 +41,8 @@ __constant__ RefTab<FAM_TET_P2> c_tab_tet2;
 __constant__ RefTab<FAM_TRI_P2_Q16> c_tab_tri2q;
 __constant__ RefTab<FAM_LINE_P1> c_tab_line1;
 __constant__ RefTab<FAM_LINE_P2> c_tab_line2;
+__constant__ RefTab<FAM_TET_P2_Q35> c_tab_tet2q;
+__constant__ RefTab<FAM_LINE_P2_Q6> c_tab_line2q;
 
 template <int F> __device__ __forceinline__ const RefTab<F>& tab();
 template <> __device__ __forceinline__ const RefTab<FAM_TRI_P1>& tab<FAM_TRI_P1>() { return c_tab_tri1; }
@@ -48,14 +52,16 @@ template <> __device__ __forceinline__ const RefTab<FAM_TET_P2>& tab<FAM_TET_P2>
 template <> __device__ __forceinline__ const RefTab<FAM_TRI_P2_Q16>& tab<FAM_TRI_P2_Q16>() { return c_tab_tri2q; }
 template <> __device__ __forceinline__ const RefTab<FAM_LINE_P1>& tab<FAM_LINE_P1>() { return c_tab_line1; }
 template <> __device__ __forceinline__ const RefTab<FAM_LINE_P2>& tab<FAM_LINE_P2>() { return c_tab_line2; }
+template <> __device__ __forceinline__ const RefTab<FAM_TET_P2_Q35>& tab<FAM_TET_P2_Q35>() { return c_tab_tet2q; }
+template <> __device__ __forceinline__ const RefTab<FAM_LINE_P2_Q6>& tab<FAM_LINE_P2_Q6>() { return c_tab_line2q; }
 
 namespace refhost {
 
 // quadrature points in reference coordinates xi (d = 2: (xi1, xi2); d = 3)
 struct Rule {
     int nq;
-    double xi[16][3];
-    double w[16];
+    double xi[35][3];
+    double w[35];
 };
 
 inline Rule rule_tri3() {
@@ -117,6 +123,28 @@ inline Rule rule_tri16() {
 inline Rule rule_line(int npts) {
     Rule r{};
     r.nq = npts;
+    if (npts == 6) {
+        // six points (reading G38): the roots t of the Legendre polynomial P_6 on [-1, 1], by Newton
+        // from Chebyshev-like starts (three-term recurrence, derivative from P_5), mapped to [0, 1];
+        // weight 1 / ((1 - t^2) P_6'(t)^2) on the unit interval
+        for (int i = 0; i < 6; ++i) {
+            double t = -std::cos(3.141592653589793238 * (i + 0.75) / 6.5);
+            double d6 = 1.0;
+            for (int it = 0; it < 60; ++it) {
+                double pm = 1.0, pc = t;  // P_0, P_1
+                for (int n = 1; n < 6; ++n) {
+                    const double pn = ((2 * n + 1) * t * pc - n * pm) / (n + 1);
+                    pm = pc;
+                    pc = pn;
+                }
+                d6 = 6.0 * (pm - t * pc) / (1.0 - t * t);  // P_6'(t) from P_5 = pm, P_6 = pc
+                t -= pc / d6;
+            }
+            r.xi[i][0] = 0.5 * (t + 1.0);
+            r.w[i] = 1.0 / ((1.0 - t * t) * d6 * d6);
+        }
+        return r;
+    }
     if (npts == 2) {
         const double h = 0.5 / std::sqrt(3.0);
         r.xi[0][0] = 0.5 - h;
@@ -161,6 +189,45 @@ inline Rule rule_tet11() {
     return r;
 }
 
+// Degree-7 fully symmetric positive tet rule, 35 points (reading G39; weights for volume 1/6):
+// centroid; (a,a,a,1-3a); (a,a,1/2-a,1/2-a); two (a,a,b,1-2a-b) orbits.  Orbits expanded here
+// in reference coordinates xi = (lambda_2, lambda_3, lambda_4).
+inline Rule rule_tet35() {
+    Rule r{};
+    r.nq = 0;
+    auto orbit = [&r](double l0, double l1, double l2, double l3, double w) {
+        double v[4] = {l0, l1, l2, l3};
+        // every distinct permutation (lexicographic enumeration of index permutations)
+        int idx[4] = {0, 1, 2, 3};
+        double seen[24][4];
+        int ns = 0;
+        do {
+            double p[4] = {v[idx[0]], v[idx[1]], v[idx[2]], v[idx[3]]};
+            bool dup = false;
+            for (int k = 0; k < ns && !dup; ++k)
+                dup = seen[k][0] == p[0] && seen[k][1] == p[1] && seen[k][2] == p[2] && seen[k][3] == p[3];
+            if (dup) continue;
+            for (int m = 0; m < 4; ++m) seen[ns][m] = p[m];
+            ++ns;
+            r.xi[r.nq][0] = p[1];
+            r.xi[r.nq][1] = p[2];
+            r.xi[r.nq][2] = p[3];
+            r.w[r.nq] = w;
+            ++r.nq;
+        } while (std::next_permutation(idx, idx + 4));
+    };
+    orbit(0.25, 0.25, 0.25, 0.25, 0.01591421491068847481009640601953773030655);
+    const double a1 = 0.315701149778202799423429999593311488426;
+    orbit(a1, a1, a1, 1.0 - 3.0 * a1, 0.00705493020166117151271436179975778958127);
+    const double a2 = 0.4495101774016036312369461770134375340242;
+    orbit(a2, a2, 0.5 - a2, 0.5 - a2, 0.005316154638809596655712470680490409516245);
+    const double a3 = 0.1888338310260010477364311038545857550051, b3 = 0.5751716375870000234832415770223075196671;
+    orbit(a3, a3, b3, 1.0 - 2.0 * a3 - b3, 0.006201188454722436894935926865246853385281);
+    const double a4 = 0.02126547254148324598883610149981994107435, b4 = 0.1466388138184849469042224171521277240548;
+    orbit(a4, a4, b4, 1.0 - 2.0 * a4 - b4, 0.001351795138317223594350572248516090026183);
+    return r;
+}
+
 // Lagrange basis at xi: values and gradients w.r.t. xi.
 // barycentric l0 = 1 - sum xi, l_k = xi_k; grad l0 = (-1,..), grad l_k = e_k.
 inline void basis_eval(int d, int order, const double* xi, double* phi, double (*dphi)[3]) {
@@ -202,24 +269,30 @@ void fill(RefTab<F>& t, const Rule& r, int d, int order) {
         double phi[10], dphi[10][3];
         basis_eval(d, order, r.xi[q], phi, dphi);
         const double x = r.xi[q][0], y = r.xi[q][1];
-        t.mono[q][0] = 1.0;
-        t.mono[q][1] = x;
-        t.mono[q][2] = y;
-        t.mono[q][3] = x * x;
-        t.mono[q][4] = x * y;
-        t.mono[q][5] = y * y;
+        constexpr int D = RefTab<F>::D;
+        if (D == 2) {
+            t.mono[D == 2 ? q : 0][0] = 1.0;
+            t.mono[D == 2 ? q : 0][1] = x;
+            t.mono[D == 2 ? q : 0][2] = y;
+            t.mono[D == 2 ? q : 0][3] = x * x;
+            t.mono[D == 2 ? q : 0][4] = x * y;
+            t.mono[D == 2 ? q : 0][5] = y * y;
+        }
         t.w[q] = r.w[q];
         for (int a = 0; a < N; ++a) {
             t.phi[q][a] = phi[a];
-            for (int m = 0; m < d; ++m) t.dphi[q][a][m] = dphi[a][m];
+            if (D == 3)
+                for (int m = 0; m < d; ++m) t.dphi[D == 3 ? q : 0][a][m] = dphi[a][m];
         }
         for (int a = 0; a < N; ++a)
             for (int b = a; b < N; ++b) {
                 const int s = sym_index(N, a, b);
                 t.pp[q][s] = phi[a] * phi[b];
-                t.gg[q][s][0] = dphi[a][0] * dphi[b][0];
-                t.gg[q][s][1] = dphi[a][0] * dphi[b][1] + dphi[a][1] * dphi[b][0];
-                t.gg[q][s][2] = dphi[a][1] * dphi[b][1];
+                if (D == 1) {
+                    t.gg[D == 1 ? q : 0][s][0] = dphi[a][0] * dphi[b][0];
+                    t.gg[D == 1 ? q : 0][s][1] = dphi[a][0] * dphi[b][1] + dphi[a][1] * dphi[b][0];
+                    t.gg[D == 1 ? q : 0][s][2] = dphi[a][1] * dphi[b][1];
+                }
             }
     }
 }

@@ -483,6 +483,12 @@ lfem_status rhs_dispatch(lfem_plan_s* p, int kind, const double* coords, const d
     case FAM_TET_P2:
         if (kll) break;
         return run_rhs<FAM_TET_P2, LFEM_RHS_LOAD>(p, coords, u, out, s);
+    case FAM_TET_P2_Q35:
+        if (kll) break;
+        return run_rhs<FAM_TET_P2_Q35, LFEM_RHS_LOAD>(p, coords, u, out, s);
+    case FAM_LINE_P2_Q6:
+        if (kll) break;
+        return run_rhs<FAM_LINE_P2_Q6, LFEM_RHS_LOAD>(p, coords, u, out, s);
     }
     return lfem_fail(LFEM_ERR_UNSUPPORTED, "right-hand side kind not available for this family");
 }

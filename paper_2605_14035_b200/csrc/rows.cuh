@@ -177,7 +177,9 @@ lfem_status rows_dispatch(lfem_plan_s* p, unsigned kinds, const double* coords, 
         p->rows_ok = h <= ROWS_SPL * 32 ? 1 : 0;
     }
     if (!p->rows_ok) return LFEM_OK;
-    if (p->mesh->family == FAM_LINE_P1 || p->mesh->family == FAM_LINE_P2) return LFEM_OK;  // -> V0
+    if (p->mesh->family == FAM_LINE_P1 || p->mesh->family == FAM_LINE_P2 || p->mesh->family == FAM_LINE_P2_Q6 ||
+        p->mesh->family == FAM_TET_P2_Q35)
+        return LFEM_OK;  // -> V0
     LFEM_TRY(rhs_prepare(p, s));
     *ok = true;
     switch (p->mesh->family) {

@@ -23,6 +23,7 @@ STATUS = {0: "LFEM_OK", 1: "LFEM_ERR_INVALID_ARG", 2: "LFEM_ERR_UNSUPPORTED", 3:
           4: "LFEM_ERR_DEGENERATE", 5: "LFEM_ERR_NOMEM", 6: "LFEM_ERR_CUDA", 7: "LFEM_ERR_STATE"}
 LFEM_SURFACE_TRI, LFEM_BULK_TET = 0, 1
 LFEM_QUAD_DEFAULT, LFEM_QUAD_TRI3_DEG2, LFEM_QUAD_TRI6_DEG4, LFEM_QUAD_TET4_DEG2, LFEM_QUAD_TET11_DEG4 = range(5)
+LFEM_QUAD_TRI16_DEG8, LFEM_QUAD_LINE2_DEG3, LFEM_QUAD_LINE3_DEG5, LFEM_QUAD_TET35_DEG7, LFEM_QUAD_LINE6_DEG11 = range(5, 10)
 LFEM_MASS, LFEM_STIFF, LFEM_STIFF_COEF = 1, 2, 4
 LFEM_NUMERIC_AUTO, LFEM_NUMERIC_V0, LFEM_NUMERIC_TILED, LFEM_NUMERIC_ROWS = 0, 1, 2, 3
 LFEM_RHS_LOAD, LFEM_RHS_KLL = 1, 2

@@ -27,11 +27,18 @@ def space_curve(n, order, seed):
     return li.Mesh(m.domain, m.order, x, m.conn, m.quad)
 
 
+def _gauss6(m):
+    """The same P2 curve with the 6-point Gauss rule (the paper's order-10 rule, reading G38)."""
+    return li.Mesh(m.domain, m.order, m.coords, m.conn, li.QUAD_LINE6_DEG11)
+
+
 CURVES = [
     ("circle1_n5", lambda: li.circle_mesh(5, 1)),
     ("circle2_n7", lambda: li.circle_mesh(7, 2)),
     ("curve1_n4000", lambda: space_curve(4000, 1, 1)),
     ("curve2_n3000", lambda: space_curve(3000, 2, 2)),
+    ("circle2_n7_gauss6", lambda: _gauss6(li.circle_mesh(7, 2))),
+    ("curve2_n3000_gauss6", lambda: _gauss6(space_curve(3000, 2, 2))),
 ]
 
 
@@ -66,3 +73,11 @@ def test_curve_tiled_and_kll_unsupported():
     with pytest.raises(lfem.LfemError) as ei:
         lfem.assemble_rhs(m, np.ones((4, m.n_nodes)), "kll")
     assert ei.value.status == 2
+
+
+def test_gauss6_load_vector_and_length():
+    m = _gauss6(space_curve(2000, 2, 5))
+    f = li.random_field(m, 9)
+    plan, b = lfem.assemble_rhs(m, f[None, :], "load")
+    o, oabs = oracle.assemble_rhs_rows(m, f[None, :], "load", with_abs=True)
+    assert np.all(np.abs(b.cpu().numpy() - o) <= 1e-12 * oabs)

@@ -32,6 +32,11 @@ def _q16(m):
     return li.Mesh(m.domain, m.order, m.coords, m.conn, li.QUAD_TRI16_DEG8, m.coeff)
 
 
+def _q35(m):
+    """The same P2 tet mesh with the 35-point degree-7 rule (the paper's degree-7 tet rule, reading G39)."""
+    return li.Mesh(m.domain, m.order, m.coords, m.conn, li.QUAD_TET35_DEG7, m.coeff)
+
+
 SMALL = [
     ("tri1_single", lambda: li.single_triangle([[0, 0, 0], [1, 0, 0], [0.2, 0.9, 0.3]], 1)),
     ("tri2_single", lambda: li.single_triangle([[0, 0, 0], [1, 0, 0], [0.2, 0.9, 0.3]], 2)),
@@ -51,6 +56,8 @@ SMALL = [
     ("C5_L4", lambda: li.make_config("C5", level_override=4)),
     ("sphere2_L3_skew_q16", lambda: _q16(_skew(li.sphere_mesh(3, 2), 3, 0.01))),
     ("C5_L4_q16", lambda: _q16(li.make_config("C5", level_override=4))),
+    ("cube2_n3_disp_q35", lambda: _q35(li.cube_mesh(3, 2, displace_seed=2))),
+    ("C4_n4_q35", lambda: _q35(li.make_config("C4", level_override=4))),
 ]
 
 
@@ -59,6 +66,11 @@ SMALL = [
 def test_parity_full(name, mk, variant):
     m = mk()
     u = m.coeff if m.coeff is not None else li.random_field(m, 11)
+    if name.endswith("_q35") and variant == lfem.LFEM_NUMERIC_TILED:
+        with pytest.raises(lfem.LfemError) as ei:  # no tile configuration for the 35-point rule
+            gpu_assemble(m, ("M", "A", "Aa"), coeff=u, variant=variant)
+        assert ei.value.status == 2
+        return
     worst, _ = check_full(m, ("M", "A", "Aa"), coeff=u, variant=variant)
     assert worst <= TOL
 

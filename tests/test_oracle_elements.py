@@ -181,14 +181,17 @@ def _exact_p2_tet(Pv):
     return np.array(M, dtype=float), np.array(A, dtype=float), float(jac) / 6.0
 
 
-def test_p2_flat_tet_exact_sympy():
+@pytest.mark.parametrize("quad", [QUAD_TET11_DEG4, 8], ids=["keast11", "deg7_35"])
+def test_p2_flat_tet_exact_sympy(quad):
+    """Affine P2 tet: M (degree 4) and A (degree 2) are integrated exactly by the 11-point
+    degree-4 rule and by the 35-point degree-7 rule (reading G39) alike."""
     Pv = [(0, 0, 0), (sp.Rational(5, 4), sp.Rational(1, 8), 0), (sp.Rational(1, 4), 1, sp.Rational(1, 8)),
           (sp.Rational(1, 8), sp.Rational(1, 4), sp.Rational(9, 8))]
     Mex, Aex, V = _exact_p2_tet(Pv)
     P = np.array([[float(c) for c in p] for p in Pv])
     pairs = [(0, 1), (1, 2), (2, 0), (0, 3), (1, 3), (2, 3)]
     X = np.concatenate([P, np.array([(P[i] + P[j]) / 2 for i, j in pairs])])
-    M, A, _ = oracle.element_matrices(BULK_TET, 2, QUAD_TET11_DEG4, X)
+    M, A, _ = oracle.element_matrices(BULK_TET, 2, quad, X)
     assert rel(M, Mex) < 1e-13
     assert rel(A, Aex) < 1e-13
     K10 = np.array([[6, 1, 1, 1, -4, -6, -4, -4, -6, -6], [1, 6, 1, 1, -4, -4, -6, -6, -4, -6],

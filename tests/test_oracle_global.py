@@ -113,6 +113,28 @@ def test_bulk_invariants_displaced_cube():
     assert abs(tr - 3.0 * vol) < 1e-12
 
 
+def test_bulk_invariants_displaced_cube_deg7_rule():
+    """Reading G39: with the 35-point degree-7 rule on curved P2 tets, det J (cubic) is integrated
+    exactly, so 1^T M 1 = 1 (G16) again; the trace identity holds for any rule; and the rule
+    differs from the 11-point one only at quadrature-error level on the curved elements."""
+    m = li.make_config("C4", level_override=3)
+    m7 = li.Mesh(m.domain, m.order, m.coords, m.conn, li.QUAD_TET35_DEG7)
+    u = li.random_field(m, 1)
+    c7 = oracle.assemble_rows(m7, ("M", "A", "Aa"), coeff=u)
+    c4 = oracle.assemble_rows(m, ("M", "A", "Aa"), coeff=u)
+    one = np.ones(m.n_nodes)
+    vol = float(one @ csr_spmv(c7, "M", one))
+    assert abs(vol - 1.0) < 1e-13
+    rowmax = np.maximum.reduceat(np.abs(c7.vals["A"]), c7.row_ptr[:-1])
+    assert np.all(np.abs(csr_spmv(c7, "A", one)) <= 1e-12 * rowmax)
+    assert np.all(np.abs(csr_spmv(c7, "Aa", one)) <= 1e-12 * np.maximum.reduceat(np.abs(c7.vals["Aa"]), c7.row_ptr[:-1]))
+    tr = sum(float(m.coords[:, k] @ csr_spmv(c7, "A", m.coords[:, k])) for k in range(3))
+    assert abs(tr - 3.0 * vol) < 1e-12
+    assert np.array_equal(c7.col_idx, c4.col_idx)
+    d = np.abs(c7.vals["A"] - c4.vals["A"]).max() / np.abs(c4.vals["A"]).max()
+    assert 1e-12 < d < 1e-2, d  # different rules, same integrand
+
+
 def test_p1_tet_cube_volume_and_trace():
     m = li.cube_mesh(3, 1, displace_seed=4)
     c = oracle.assemble_rows(m, ("M", "A"))

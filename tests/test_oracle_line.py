@@ -17,14 +17,15 @@ import lfem_inputs as li
 import oracle
 
 
-@pytest.mark.parametrize("quad,deg,npts", [(li.QUAD_LINE2_DEG3, 3, 2), (li.QUAD_LINE3_DEG5, 5, 3)])
+@pytest.mark.parametrize("quad,deg,npts", [(li.QUAD_LINE2_DEG3, 3, 2), (li.QUAD_LINE3_DEG5, 5, 3),
+                                            (li.QUAD_LINE6_DEG11, 11, 6)])
 def test_gauss_rules(quad, deg, npts):
     lam, w = oracle.rule(quad)
     assert lam.shape[0] == npts and abs(w.sum() - 1.0) < 1e-15
     xi = lam[:, 1]
     for k in range(deg + 1):
         assert abs(np.sum(w * xi ** k) - 1.0 / (k + 1)) < 1e-15
-    assert abs(np.sum(w * xi ** (deg + 1)) - 1.0 / (deg + 2)) > 1e-6
+    assert abs(np.sum(w * xi ** (deg + 1)) - 1.0 / (deg + 2)) > 1e-9
 
 
 @pytest.mark.parametrize("order", [1, 2])
@@ -58,10 +59,12 @@ def test_circle_p1_polygon_length(n):
     assert abs(tr - M.sum()) < 1e-12 * M.sum()
 
 
-def test_circle_p2_length_eoc_and_trace():
+@pytest.mark.parametrize("quad", [li.QUAD_LINE3_DEG5, li.QUAD_LINE6_DEG11], ids=["gauss3", "gauss6"])
+def test_circle_p2_length_eoc_and_trace(quad):
     errs = []
     for n in (8, 16, 32):
         m = li.circle_mesh(n, 2)
+        m.quad = quad
         M, A = _dense(m, "M"), _dense(m, "A")
         errs.append(abs(M.sum() - 2 * math.pi))
         assert np.max(np.abs(A.sum(axis=1))) < 1e-11 * np.max(np.abs(A))

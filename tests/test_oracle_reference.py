@@ -96,7 +96,7 @@ def test_triangle_rule_exactness(quad, deg, npts):
     assert max(errs) > 1e-8
 
 
-@pytest.mark.parametrize("quad,deg,npts", [(QUAD_TET4_DEG2, 2, 4), (QUAD_TET11_DEG4, 4, 11)])
+@pytest.mark.parametrize("quad,deg,npts", [(QUAD_TET4_DEG2, 2, 4), (QUAD_TET11_DEG4, 4, 11), (8, 7, 35)])
 def test_tet_rule_exactness(quad, deg, npts):
     lam, w = oracle.rule(quad)
     assert lam.shape[0] == npts
@@ -114,3 +114,16 @@ def test_tet_rule_exactness(quad, deg, npts):
     assert max(errs) > 1e-8
     if quad == QUAD_TET11_DEG4:
         assert w.min() < 0  # reading G8: Keast's centroid weight is negative
+
+
+def test_tet35_rule_positive_interior_symmetric():
+    """Reading G39 (the paper's degree-7 tet rule): every weight positive, every point
+    interior, and the point set invariant under all 24 permutations of the barycentrics
+    (a fully symmetric rule), weights equal on each orbit."""
+    lam, w = oracle.rule(8)
+    assert w.min() > 0 and lam.min() > 0
+    key = {tuple(np.round(l, 14)): wi for l, wi in zip(lam, w)}
+    for l, wi in zip(lam, w):
+        for perm in itertools.permutations(range(4)):
+            k = tuple(np.round(l[list(perm)], 14))
+            assert k in key and abs(key[k] - wi) < 1e-18
