@@ -46,6 +46,12 @@ struct lfem_mesh_s {
     const int32_t* conn;
 };
 
+// Slot words of the tiled kernel: a missing second contribution is encoded as the
+// stage's zero word (1) or as 0xffff with a predicated load (0).
+#ifndef LFEM_ZERO_WORD
+#define LFEM_ZERO_WORD 1
+#endif
+
 // Row-tile plan of the fused numeric kernel (tiles.cu).
 struct TilePlan {
     int n_tiles = 0;

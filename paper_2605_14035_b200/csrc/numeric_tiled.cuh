@@ -138,9 +138,11 @@ struct TileLayout {
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 // stage[2] | meta[3] = {conn16 | pairs | heavy | halo} | nodes[2] = {xyz | u}
 __host__ __device__ inline TileLayout tile_layout(int nsym, int nref, int maxe, int slots_cap, int heavy_cap,
-                                                  int nodes_cap) {
+                                                  int nodes_cap, int heavy_words) {
     TileLayout L;
-    L.stage_bytes = align16(sizeof(double) * (size_t)nsym * maxe);
+    // stage: nsym x maxe entries, then the tail: a zero word
+    (void)heavy_words;
+    L.stage_bytes = align16(sizeof(double) * ((size_t)nsym * maxe + 1));
     L.conn_off = 0;
     L.pairs_off = align16(sizeof(uint16_t) * ((size_t)maxe * nref + 8));
     L.heavy_off = L.pairs_off + align16(sizeof(uint32_t) * ((size_t)slots_cap + 8));
@@ -292,7 +294,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int G = gridDim.x;
-    const TileLayout lay = tile_layout(E::NS, N, a.maxe, a.slots_cap, a.heavy_cap, a.nodes_cap);
+    const TileLayout lay = tile_layout(E::NS, N, a.maxe, a.slots_cap, a.heavy_cap, a.nodes_cap, a.heavy_words);
+    const int tail_dbl = E::NS * a.maxe;  // stage tail: the zero word
     const int stage_dbl = (int)(lay.stage_bytes / sizeof(double));
     // buffer bases by arithmetic (a dynamically indexed member array would live in local memory)
     const size_t meta0 = lay.meta_off[0], meta_stride = lay.meta_off[1] - lay.meta_off[0];
@@ -312,6 +315,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
             mbar_init(&node_empty[b], CT);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int b = 0; b < LFEM_NSB; ++b) tile_smem_d[b * stage_dbl + tail_dbl] = 0.0;  // never written again
     }
     __syncthreads();
     if (tid == CT) {
@@ -380,17 +384,20 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
         }
     } else {
         // ------------------------------------------------------------ reduce warps (+ producer)
-        // Light slots (1-2 contributions) in units of two consecutive CSR slots (absolute
-        // index 2u, 2u+1): one 8-B load of the two slot words, four stage loads, one
-        // 16-B streaming store; consecutive threads take consecutive units (512-B
-        // coalesced stores per warp).  Slot words hold stage BYTE offsets.  One compact
-        // loop serves every kind (the kinds' code is not replicated: instruction-cache
-        // footprint).  Heavy entries: one per thread, loads in parallel, summed in order.
+        // Per kind: (1) every CSR slot of the tile in units of two consecutive slots
+        // (absolute index 2u, 2u+1): one 8-B load of the two slot words, four stage loads
+        // (byte offsets; a missing second contribution is the stage's zero word), one 16-B
+        // streaming store -- no case analysis in the loop (a heavy slot's word points at the
+        // zero word: 0 is written); consecutive threads take consecutive units (512-B
+        // coalesced stores per warp); an odd first / last slot of the tile is done apart.
+        // (2) a named barrier of the reduce warps (orders the heavy slots' second store
+        // after the first); (3) the heavy slots: one fixed-size entry per thread, loads in
+        // parallel, summed in order.  One compact loop serves every kind (instruction-cache
+        // footprint).
         if (Cfg::REGS_R) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_R));
         constexpr int RT = RW * 32;
         constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
-        const int rw = warp - CW, rt = tid - CT;
-        (void)rw;
+        const int rt = tid - CT;
         uint32_t pass = 0;
         for (int it = 0, t = blockIdx.x; t < a.n_tiles; ++it, t += G) {
             const int b = it % LFEM_NMB;
@@ -403,7 +410,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
             const int p0 = s0 & ~3;
             const int hw = a.heavy_words, nent = (LFEM_TILED_SKIP & 2) ? 0 : i1.w / hw;
             const uint16_t* s_heavy = reinterpret_cast<const uint16_t*>(mb + lay.heavy_off);
-            const int u0 = s0 >> 1, u1 = (se + 1) >> 1;
+            const int uA = (s0 + 1) >> 1, uB = se >> 1;  // units with both slots in [s0, se)
 #pragma unroll 1
             for (int kk = 0; kk < NK; ++kk) {
                 const int kind = DM ? (kk == 0 ? KIND_M : (DA && kk == 1) ? KIND_A : KIND_AA)
@@ -412,28 +419,23 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 mbar_wait(&stage_full[sb], (pass / LFEM_NSB) & 1);
                 const unsigned char* st = reinterpret_cast<const unsigned char*>(tile_smem_d + sb * stage_dbl);
                 double* out = a.v[kind];
-#pragma unroll 2
-                for (int u = u0 + rt; u < u1; u += RT) {
-                    const int sa = 2 * u;
-                    const uint2 w = *reinterpret_cast<const uint2*>(s_pw + (sa - p0));
-                    // a word outside the tile's range, or a heavy slot, is not written here
-                    const bool ok0 = sa >= s0 && w.x != 0xffffffffu;
-                    const bool ok1 = sa + 1 < se && w.y != 0xffffffffu;
-                    const uint32_t a0 = w.x & 0xffffu, b0 = w.x >> 16, a1 = w.y & 0xffffu, b1 = w.y >> 16;
-                    const double x00 = ok0 ? *reinterpret_cast<const double*>(st + a0) : 0.0;
-                    const double x01 = ok0 && b0 != 0xffffu ? *reinterpret_cast<const double*>(st + b0) : 0.0;
-                    const double x10 = ok1 ? *reinterpret_cast<const double*>(st + a1) : 0.0;
-                    const double x11 = ok1 && b1 != 0xffffu ? *reinterpret_cast<const double*>(st + b1) : 0.0;
+                auto slot_value = [&](uint32_t w) {
                     // (0 + x0) + x1: the order of V0 and the oracle; + 0.0 is exact (sums are never -0)
-                    const double v0 = (0.0 + x00) + x01, v1 = (0.0 + x10) + x11;
-                    if (ok0 && ok1) {
-                        asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(out + sa), "d"(v0), "d"(v1) : "memory");
-                    } else {
-                        if (ok0) st_stream(out + sa, v0);
-                        if (ok1) st_stream(out + sa + 1, v1);
-                    }
+                    const double x0 = *reinterpret_cast<const double*>(st + (w & 0xffffu));
+                    const uint32_t c1 = w >> 16;
+                    const double x1 = (LFEM_ZERO_WORD || c1 != 0xffffu) ? *reinterpret_cast<const double*>(st + c1) : 0.0;
+                    return (0.0 + x0) + x1;
+                };
+#pragma unroll 2
+                for (int u = uA + rt; u < uB; u += RT) {
+                    const uint2 w = *reinterpret_cast<const uint2*>(s_pw + (2 * u - p0));
+                    const double v0 = slot_value(w.x), v1 = slot_value(w.y);
+                    asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(out + 2 * u), "d"(v0), "d"(v1) : "memory");
                 }
-                // heavy slots: one fixed-size entry per thread, loads in parallel, summed in order
+                // (s0 odd and se odd exclude each other when ns = 1: the two edge slots never coincide)
+                if (rt == 0 && (s0 & 1) && ns > 0) st_stream(out + s0, slot_value(s_pw[s0 - p0]));
+                if (rt == 1 && (se & 1) && ns > 0) st_stream(out + se - 1, slot_value(s_pw[se - 1 - p0]));
+                if (nent > 0) asm volatile("bar.sync 1, %0;" ::"n"(RT) : "memory");  // heavy stores land last
                 for (int h = rt; h < nent; h += RT) {
                     const uint4* ent = reinterpret_cast<const uint4*>(s_heavy + h * hw);
                     const uint4 w0 = ent[0];
@@ -442,8 +444,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                                            w0.w & 0xffffu, w0.w >> 16};
                     double x[6];
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) x[k] = c[k] != 0xffffu ? *reinterpret_cast<const double*>(st + c[k]) : 0.0;
-                    double v = 0.0;
+                    for (int k = 0; k < 6; ++k) x[k] = *reinterpret_cast<const double*>(st + c[k]);
+                    double v = 0.0;  // never -0: adding the zero word of unused codes is exact
 #pragma unroll
                     for (int k = 0; k < 6; ++k) v = v + x[k];
                     for (int blk = 1; 6 + 8 * (blk - 1) < cnt; ++blk) {
@@ -452,8 +454,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                                                w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
                         double y[8];
 #pragma unroll
-                        for (int k = 0; k < 8; ++k)
-                            y[k] = d[k] != 0xffffu ? *reinterpret_cast<const double*>(st + d[k]) : 0.0;
+                        for (int k = 0; k < 8; ++k) y[k] = *reinterpret_cast<const double*>(st + d[k]);
 #pragma unroll
                         for (int k = 0; k < 8; ++k) v = v + y[k];
                     }
@@ -485,7 +486,7 @@ constexpr int tile_capacity() {
 template <int F>
 size_t tile_smem_bytes(const TilePlan& T) {
     return tile_layout(FamInfo<F>::NSYM, FamInfo<F>::NREF, T.max_tile_elems, T.max_tile_slots, T.max_tile_heavy,
-                       T.max_tile_nodes)
+                       T.max_tile_nodes, T.heavy_words)
         .total;
 }
 

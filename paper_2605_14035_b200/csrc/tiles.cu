@@ -177,7 +177,12 @@ __global__ void k_row_heavy(int64_t n_rows, const int64_t* __restrict__ row_ptr,
     }
 }
 
-// per row: the slot words and heavy entries (see the header)
+// per row: the slot words and heavy entries (see the header).  Stage tail (byte offset
+// tail = 8 nsym maxe of every stage buffer): a zero word.  A light slot with one
+// contribution has c1 = tail (LFEM_ZERO_WORD) or 0xffff; a heavy slot's word is
+// (tail, tail): the kernel's light loop writes 0 there, then (after a barrier of the
+// reduce warps) the heavy loop writes the slot's sum -- no case analysis in the light
+// loop.  Unused codes of a heavy entry are the zero word.
 __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of, const int64_t* __restrict__ bounds,
                              int hw, int nsym, int maxe,
                              const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ slot_ptr,
@@ -185,23 +190,26 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
                              const int32_t* __restrict__ telems, const uint16_t* __restrict__ tpos,
                              const int64_t* __restrict__ hptr, uint32_t* __restrict__ pairs,
                              uint16_t* __restrict__ heavy, int* __restrict__ bad) {
+    const int64_t tail = 8 * (int64_t)nsym * maxe;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x) {
         const int t = tile_of[r];
         const int32_t* te = telems + tptr[t];
         const int ne = (int)(tptr[t + 1] - tptr[t]);
         const int64_t sbase = row_ptr[bounds[t]];
+        const int64_t hbase = hptr[bounds[t]];  // the tile's first heavy entry
         int64_t cur = hptr[r] * hw;
         for (int64_t s = row_ptr[r]; s < row_ptr[r + 1]; ++s) {
             const int j0 = slot_ptr[s], j1 = slot_ptr[s + 1];
             const int c = j1 - j0;
-            uint32_t code[2] = {0xffffu, 0xffffu};
+            uint32_t code[2] = {(uint32_t)tail, LFEM_ZERO_WORD ? (uint32_t)tail : 0xffffu};
             const bool hv = c > 2;
+            (void)hbase;
             if (hv) {
                 if (s - sbase >= 0xffff) atomicExch(bad, 3);
-                pairs[s] = 0xffffffffu;
+                pairs[s] = (uint32_t)tail | ((LFEM_ZERO_WORD ? (uint32_t)tail : 0xffffu) << 16);
                 heavy[cur] = (uint16_t)(s - sbase);
                 heavy[cur + 1] = (uint16_t)c;
-                for (int k = c; k < hw - 2; ++k) heavy[cur + 2 + k] = 0xffffu;
+                for (int k = c; k < hw - 2; ++k) heavy[cur + 2 + k] = (uint16_t)tail;
             }
             for (int j = j0; j < j1; ++j) {
                 const int32_t cc = codes[j];
@@ -222,6 +230,13 @@ __global__ void k_tile_pairs(int64_t n_rows, const int32_t* __restrict__ tile_of
             else pairs[s] = code[0] | (code[1] << 16);
         }
     }
+}
+
+// max heavy entries of a tile (the stage tail must fit the 16-bit byte offsets)
+__global__ void k_tile_heavymax(int n_tiles, const int64_t* __restrict__ bounds, const int64_t* __restrict__ hptr,
+                                int* __restrict__ maxh) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n_tiles; t += gridDim.x * blockDim.x)
+        atomicMax(maxh, (int)(hptr[bounds[t + 1]] - hptr[bounds[t]]));
 }
 
 // Per tile: its halo nodes (nodes of its elements outside its rows; sorted,
@@ -661,6 +676,14 @@ lfem_status build_tiles(lfem_plan_s* p, int emax, cudaStream_t s) {
     if (hw > 256) return lfem_fail(LFEM_ERR_UNSUPPORTED, "a CSR slot has more than 254 contributions");
     T.heavy_words = hw;
     if (heavy_slots * hw >= INT_MAX) return lfem_fail(LFEM_ERR_UNSUPPORTED, "heavy lists >= 2^31 entries");
+    // the stage tail (zero word + heavy sums) must stay addressable by 16-bit byte offsets
+    LFEM_CUDA(cudaMemsetAsync(flags, 0, sizeof(int) * 4, s));
+    k_tile_heavymax<<<grid_for(n_tiles, 256), 256, 0, s>>>(n_tiles, bounds, hptr, flags);
+    LFEM_CUDA(cudaGetLastError());
+    int maxh = 0;
+    LFEM_CUDA(cudaMemcpyAsync(&maxh, flags, sizeof(int), cudaMemcpyDeviceToHost, s));
+    LFEM_CUDA(cudaStreamSynchronize(s));
+    if (8 * ((int64_t)p->mesh->nsym * maxe + 1) >= 0xfff0) return LFEM_OK;  // not ready: lower the budget
     // TMA bulk copies round each tile's ranges out to 16 B: pad both arrays
     LFEM_TRY(dev_alloc_t(&T.pairs, p->nnz + 8, s));
     LFEM_TRY(dev_alloc_t(&T.heavy, heavy_slots * hw + 16, s));
