@@ -52,10 +52,10 @@
 #define LFEM_P2_EPT 1
 #endif
 #ifndef LFEM_REGS_C
-#define LFEM_REGS_C 168
+#define LFEM_REGS_C 176
 #endif
 #ifndef LFEM_REGS_R
-#define LFEM_REGS_R 88
+#define LFEM_REGS_R 80
 #endif
 #ifndef LFEM_NMB  // tile metadata buffers (tiles in flight ahead of the compute warps)
 #define LFEM_NMB 3
