@@ -420,11 +420,12 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 const unsigned char* st = reinterpret_cast<const unsigned char*>(tile_smem_d + sb * stage_dbl);
                 double* out = a.v[kind];
                 auto slot_value = [&](uint32_t w) {
-                    // (0 + x0) + x1: the order of V0 and the oracle; + 0.0 is exact (sums are never -0)
+                    // x0 + x1 in the symbolic order (reading G21); for one contribution x1 = +0 (the
+                    // oracle's 0 + x0: the same value, -0 becomes +0 in both)
                     const double x0 = *reinterpret_cast<const double*>(st + (w & 0xffffu));
                     const uint32_t c1 = w >> 16;
                     const double x1 = (LFEM_ZERO_WORD || c1 != 0xffffu) ? *reinterpret_cast<const double*>(st + c1) : 0.0;
-                    return (0.0 + x0) + x1;
+                    return x0 + x1;
                 };
 #pragma unroll 2
                 for (int u = uA + rt; u < uB; u += RT) {
