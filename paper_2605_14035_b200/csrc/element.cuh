@@ -31,6 +31,11 @@
 #pragma once
 #include "lfem_internal.cuh"
 #include "reference.cuh"
+#include "tet_moments.cuh"
+
+#ifndef LFEM_TET_MOMENTS  // P2 tet stiffness in moment form (1) or gradient form (0)
+#define LFEM_TET_MOMENTS 0
+#endif
 
 // Coefficients of the reference shape-function derivatives (small integers):
 //   d phi_j / d xi_m (xi) = SA(j,m) + sum_n SB(j,m,n) xi_n
@@ -433,6 +438,38 @@ struct Elem {
                     }
                 sink(s, v);
             }
+        } else if constexpr (N == 10 && LFEM_TET_MOMENTS) {
+            // P2 tets, moment form (tet_moments.cuh, generated): per point the symmetric
+            // K_q = (w_q / |det J|) cof^T cof (6 entries), accumulated against the 10 monomials
+            // of degree <= 2 of xi_q; the 55 entries are integer combinations of the 60 moments
+            // (741 terms) -- 38 % fewer FP64 operations than the gradient form below.
+            double mom[6][10];
+#pragma unroll
+            for (int c = 0; c < 6; ++c)
+#pragma unroll
+                for (int al = 0; al < 10; ++al) mom[c][al] = 0.0;
+#pragma unroll QU
+            for (int q = 0; q < NQ; ++q) {
+                double J[3][D], C[3][3];
+                jac_at(g.J0, g.J1, q, J);
+                const double adet = fabs(cof(J, C));
+                double c = T.w[q] * rcp_nr(adet);
+                if (COEF) c = c * g.aq[q];
+                double K[6];
+                constexpr int KM[6] = {0, 1, 2, 0, 0, 1}, KN[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    double v = C[0][KM[i]] * C[0][KN[i]];
+                    v = fma(C[1][KM[i]], C[1][KN[i]], v);
+                    v = fma(C[2][KM[i]], C[2][KN[i]], v);
+                    K[i] = c * v;
+                }
+#pragma unroll
+                for (int i = 0; i < 6; ++i)
+#pragma unroll
+                    for (int al = 0; al < 10; ++al) mom[i][al] = fma(K[i], T.mono3[D == 3 ? q : 0][al], mom[i][al]);
+            }
+            tet_moment_combine(mom, sink);
         } else {
             double acc[NS];
 #pragma unroll

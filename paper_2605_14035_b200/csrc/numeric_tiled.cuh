@@ -550,6 +550,15 @@ lfem_status run_tiled(lfem_plan_s* p, const double* coords, const double* coeff,
     int occ = 0;
     LFEM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_tiled<F, DM, DA, DAA>, THREADS, smem));
     if (occ < 1) return lfem_fail(LFEM_ERR_UNSUPPORTED, "tiled kernel does not fit on an SM");
+    if (TileCfg<F>::REGS_C || TileCfg<F>::REGS_R) {
+        // setmaxnreg moves registers inside the CTA's launch allocation: an increase that does not
+        // fit would block forever, so refuse such a configuration instead of launching it
+        cudaFuncAttributes fa{};
+        LFEM_CUDA(cudaFuncGetAttributes(&fa, k_tiled<F, DM, DA, DAA>));
+        const long need = 32L * (TileCfg<F>::CW * TileCfg<F>::REGS_C + TileCfg<F>::RW * TileCfg<F>::REGS_R);
+        if (need > (long)THREADS * ((fa.numRegs + 7) / 8 * 8))
+            return lfem_fail(LFEM_ERR_UNSUPPORTED, "tiled kernel register split exceeds the CTA's allocation");
+    }
     TileArgs a;
     a.n_tiles = T.n_tiles;
     a.maxe = T.max_tile_elems;

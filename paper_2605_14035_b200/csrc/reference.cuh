@@ -32,6 +32,7 @@ struct RefTab {
     double pp[NQ][NSYM];
     double gg[D == 1 ? NQ : 1][NSYM][3];     // curves (metric form)
     double mono[D == 2 ? NQ : 1][6];         // surfaces: 1, x, y, x^2, x y, y^2 at xi_q (stiffness moments)
+    double mono3[D == 3 ? NQ : 1][10];       // P2 tets: 1, x, y, z, xx, xy, xz, yy, yz, zz at xi_q
 };
 
 __constant__ RefTab<FAM_TRI_P1> c_tab_tri1;
@@ -277,6 +278,11 @@ void fill(RefTab<F>& t, const Rule& r, int d, int order) {
             t.mono[D == 2 ? q : 0][3] = x * x;
             t.mono[D == 2 ? q : 0][4] = x * y;
             t.mono[D == 2 ? q : 0][5] = y * y;
+        }
+        if (D == 3) {
+            const double z = r.xi[q][2];
+            const double m3[10] = {1.0, x, y, z, x * x, x * y, x * z, y * y, y * z, z * z};
+            for (int al = 0; al < 10; ++al) t.mono3[D == 3 ? q : 0][al] = m3[al];
         }
         t.w[q] = r.w[q];
         for (int a = 0; a < N; ++a) {
