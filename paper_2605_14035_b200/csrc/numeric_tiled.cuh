@@ -109,6 +109,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
     } while (!done);
 }
 
+// Poison mode (compile-time -DLFEM_TILED_POISON=1, tests only; compute-sanitizer is closed on
+// this pool): every shared-memory buffer is overwritten with a poison pattern (NaN doubles /
+// 0xff bytes) as soon as its consumers are done with it, before it is handed back to its
+// producer.  A read that raced ahead of a producer (a missing mbarrier wait, async-proxy
+// ordering, a stale TMA buffer) or a code word pointing at an unwritten position then yields
+// NaN or a wrong value, which the parity tests catch.
+#ifndef LFEM_TILED_POISON
+#define LFEM_TILED_POISON 0
+#endif
+
 // timing experiments only (compile-time, scripts/build_variants.py -DLFEM_TILED_SKIP=..):
 // bit0 compute warps skip the kind contractions, bit1 reduce warps skip the slots
 #ifndef LFEM_TILED_SKIP
@@ -343,6 +353,11 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
             mbar_wait(&node_full[nb], (it >> 1) & 1);
             read_nodes<F, DAA, EPT>(i2, reinterpret_cast<const uint16_t*>(smem + meta0 + b * meta_stride + lay.conn_off),
                                     smem + node0 + nb * node_stride, lay, ne, tid, CT, X, U);
+            if (LFEM_TILED_POISON) {  // every compute thread has read its nodes: poison the node buffer
+                asm volatile("bar.sync 2, %0;" ::"n"(CT) : "memory");
+                double* nbuf = reinterpret_cast<double*>(smem + node0 + nb * node_stride);
+                for (int i = tid; i < (int)(lay.node_bytes / sizeof(double)); i += CT) nbuf[i] = __longlong_as_double(-1LL);
+            }
             mbar_arrive(&node_empty[nb]);
             typename E::Geo geo[EPT];
 #pragma unroll
@@ -461,6 +476,12 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                     }
                     st_stream(out + s0 + (w0.x & 0xffffu), v);
                 }
+                if (LFEM_TILED_POISON) {  // every reduce thread has read the stage: poison it (not the zero word)
+                    asm volatile("bar.sync 1, %0;" ::"n"(RT) : "memory");
+                    double* sw = tile_smem_d + sb * stage_dbl;
+                    for (int i = rt; i < tail_dbl; i += RT) sw[i] = __longlong_as_double(-1LL);
+                    asm volatile("bar.sync 1, %0;" ::"n"(RT) : "memory");
+                }
                 mbar_arrive(&stage_empty[sb]);
                 ++pass;
             }
@@ -472,6 +493,10 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 if (done == RW - 1) {
                     meta_done[b] = 0;
                     __threadfence_block();
+                    if (LFEM_TILED_POISON) {  // the tile's compute and reduce are done with meta buffer b
+                        uint4* mw = reinterpret_cast<uint4*>(smem + meta0 + b * meta_stride);
+                        for (int i = 0; i < (int)(lay.meta_bytes / 16); ++i) mw[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+                    }
                     if (t + LFEM_NMB * G < a.n_tiles) issue_tile(a, smem, lay, t + LFEM_NMB * G, b, sinfo, meta_full);
                 }
             }
