@@ -57,6 +57,12 @@
 #ifndef LFEM_REGS_R
 #define LFEM_REGS_R 80
 #endif
+#ifndef LFEM_RUN  // reduce loop unroll (two-slot units)
+#define LFEM_RUN 2
+#endif
+#ifndef LFEM_HEAVY_REGS  // heavy entries per reduce thread summed into registers before the light loop
+#define LFEM_HEAVY_REGS 0
+#endif
 #ifndef LFEM_NMB  // tile metadata buffers (tiles in flight ahead of the compute warps)
 #define LFEM_NMB 3
 #endif
@@ -412,6 +418,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
         if (Cfg::REGS_R) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(Cfg::REGS_R));
         constexpr int RT = RW * 32;
         constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
+        constexpr int HK = LFEM_HEAVY_REGS;  // heavy entries per thread summed before the light loop
+        constexpr int RUN = LFEM_RUN;        // (a macro is not expanded inside #pragma unroll)
         const int rt = tid - CT;
         uint32_t pass = 0;
         for (int it = 0, t = blockIdx.x; t < a.n_tiles; ++it, t += G) {
@@ -434,6 +442,34 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 mbar_wait(&stage_full[sb], (pass / LFEM_NSB) & 1);
                 const unsigned char* st = reinterpret_cast<const unsigned char*>(tile_smem_d + sb * stage_dbl);
                 double* out = a.v[kind];
+                // heavy entry h: [slot - s0, count, codes...], summed in order (never -0: adding the
+                // zero word of unused codes is exact)
+                auto heavy_sum = [&](int h, int& slot) {
+                    const uint4* ent = reinterpret_cast<const uint4*>(s_heavy + h * hw);
+                    const uint4 w0 = ent[0];
+                    const int cnt = (int)(w0.x >> 16);
+                    slot = (int)(w0.x & 0xffffu);
+                    const uint32_t c[6] = {w0.y & 0xffffu, w0.y >> 16, w0.z & 0xffffu, w0.z >> 16,
+                                           w0.w & 0xffffu, w0.w >> 16};
+                    double x[6];
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) x[k] = *reinterpret_cast<const double*>(st + c[k]);
+                    double v = 0.0;
+#pragma unroll
+                    for (int k = 0; k < 6; ++k) v = v + x[k];
+                    for (int blk = 1; 6 + 8 * (blk - 1) < cnt; ++blk) {
+                        const uint4 w = ent[blk];
+                        const uint32_t d[8] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16,
+                                               w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
+                        double y[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+                            y[k] = *reinterpret_cast<const double*>(st + d[k]);
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) v = v + y[k];
+                    }
+                    return v;
+                };
                 auto slot_value = [&](uint32_t w) {
                     // x0 + x1 in the symbolic order (reading G21); for one contribution x1 = +0 (the
                     // oracle's 0 + x0: the same value, -0 becomes +0 in both)
@@ -442,7 +478,17 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                     const double x1 = (LFEM_ZERO_WORD || c1 != 0xffffu) ? *reinterpret_cast<const double*>(st + c1) : 0.0;
                     return x0 + x1;
                 };
-#pragma unroll 2
+                // heavy sums first (their loads overlap the light loop; the stores wait for the barrier)
+                double hval[HK > 0 ? HK : 1];
+                int hslot[HK > 0 ? HK : 1];
+#pragma unroll
+                for (int k = 0; k < HK; ++k) {
+                    const int h = rt + k * RT;
+                    hslot[k] = -1;
+                    hval[k] = 0.0;
+                    if (h < nent) hval[k] = heavy_sum(h, hslot[k]);
+                }
+#pragma unroll RUN
                 for (int u = uA + rt; u < uB; u += RT) {
                     const uint2 w = *reinterpret_cast<const uint2*>(s_pw + (2 * u - p0));
                     const double v0 = slot_value(w.x), v1 = slot_value(w.y);
@@ -452,29 +498,13 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 if (rt == 0 && (s0 & 1) && ns > 0) st_stream(out + s0, slot_value(s_pw[s0 - p0]));
                 if (rt == 1 && (se & 1) && ns > 0) st_stream(out + se - 1, slot_value(s_pw[se - 1 - p0]));
                 if (nent > 0) asm volatile("bar.sync 1, %0;" ::"n"(RT) : "memory");  // heavy stores land last
-                for (int h = rt; h < nent; h += RT) {
-                    const uint4* ent = reinterpret_cast<const uint4*>(s_heavy + h * hw);
-                    const uint4 w0 = ent[0];
-                    const int cnt = (int)(w0.x >> 16);
-                    const uint32_t c[6] = {w0.y & 0xffffu, w0.y >> 16, w0.z & 0xffffu, w0.z >> 16,
-                                           w0.w & 0xffffu, w0.w >> 16};
-                    double x[6];
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) x[k] = *reinterpret_cast<const double*>(st + c[k]);
-                    double v = 0.0;  // never -0: adding the zero word of unused codes is exact
-#pragma unroll
-                    for (int k = 0; k < 6; ++k) v = v + x[k];
-                    for (int blk = 1; 6 + 8 * (blk - 1) < cnt; ++blk) {
-                        const uint4 w = ent[blk];
-                        const uint32_t d[8] = {w.x & 0xffffu, w.x >> 16, w.y & 0xffffu, w.y >> 16,
-                                               w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
-                        double y[8];
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) y[k] = *reinterpret_cast<const double*>(st + d[k]);
-#pragma unroll
-                        for (int k = 0; k < 8; ++k) v = v + y[k];
-                    }
-                    st_stream(out + s0 + (w0.x & 0xffffu), v);
+                for (int k = 0; k < HK; ++k)
+                    if (hslot[k] >= 0) st_stream(out + s0 + hslot[k], hval[k]);
+                for (int h = rt + HK * RT; h < nent; h += RT) {  // beyond the register-held entries
+                    int sl;
+                    const double v = heavy_sum(h, sl);
+                    st_stream(out + s0 + sl, v);
                 }
                 if (LFEM_TILED_POISON) {  // every reduce thread has read the stage: poison it (not the zero word)
                     asm volatile("bar.sync 1, %0;" ::"n"(RT) : "memory");

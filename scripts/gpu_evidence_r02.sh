@@ -35,9 +35,20 @@ if [ -z "$SKIP_NCU" ]; then
     $CMDF > gpurun_out/${TAG}_plain_$cfg.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:k_tiled -s 3 -c 1 -o gpurun_out/${TAG}_${cfg}_full $CMDF > gpurun_out/${TAG}_ncu_full_$cfg.log 2>&1
     echo "ncu full $cfg exit $?"
+    # summarise here (the reports exceed what gpurun brings back), keep the text only
+    LCSV=-; [ $cfg = C5 ] && LCSV=gpurun_out/${TAG}_launches.csv
+    python scripts/ncu_summary.py gpurun_out/${TAG}_${cfg}_full.ncu-rep $LCSV gpurun_out/profiles_${TAG} $cfg > /dev/null 2>&1
+    ncu -i gpurun_out/${TAG}_${cfg}_full.ncu-rep --page raw --csv > gpurun_out/profiles_${TAG}/ncu_${cfg}_raw.csv 2>/dev/null
+    rm -f gpurun_out/${TAG}_${cfg}_full.ncu-rep
   done
   CMD4="python bench.py --config C4 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e"
   $CMD4 > gpurun_out/${TAG}_plain_C4.log 2>&1 && \
   ncu --set full --clock-control none --import-source on -k regex:"${C4_KERNELS:-k_elem_v0|k_slot_reduce}" -s ${C4_SKIP:-6} -c ${C4_COUNT:-2} -o gpurun_out/${TAG}_C4_full $CMD4 > gpurun_out/${TAG}_ncu_full_C4.log 2>&1
   echo "ncu full C4 exit $?"
+  for row in 0 1; do
+    NCU_KERNEL_ROW=$row python scripts/ncu_summary.py gpurun_out/${TAG}_C4_full.ncu-rep - gpurun_out/profiles_${TAG} C4 > /dev/null 2>&1
+  done
+  ncu -i gpurun_out/${TAG}_C4_full.ncu-rep --page raw --csv > gpurun_out/profiles_${TAG}/ncu_C4_raw.csv 2>/dev/null
+  rm -f gpurun_out/${TAG}_C4_full.ncu-rep
+  du -sh gpurun_out
 fi
