@@ -84,7 +84,8 @@ def l2_note(name):
 
 def config_matrices(name, m, kinds, world, variant):
     """The bench line's `config` (identical in the GPU arm and the reference arm)."""
-    return {"workload": f"{name}: {CONFIG_DESC[name]}" + (" [Dunavant-8 rule, 16 points]" if QUAD8 else ""),
+    return {"workload": f"{name}: {CONFIG_DESC[name]}" + (" [Dunavant-8 rule, 16 points]" if QUAD8 else "")
+                        + (" [natural generator order, no SFC renumbering]" if NATURAL else ""),
             "kinds": list(kinds), "n_elems": int(m.n_elems), "n_nodes": int(m.n_nodes),
             "parallelism": f"row-blocks x{world}", "l2": l2_note(name), "variant": variant}
 
@@ -96,12 +97,16 @@ def config_rhs(name, m, kind, nc, world, variant):
 
 
 QUAD8 = False  # --quad8: P2 triangle configs with Dunavant's 16-point degree-8 rule
+NATURAL = False  # --natural: C2 in the generator's own numbering (SURVEY §8(d).2 sensitivity point)
+CPU_THREADS = None  # --cpu-threads: threads of the oracle's cpu_baseline sample (default: all host cores)
 
 
 def build_mesh(name):
     import lfem_inputs as li
     t0 = time.time()
-    m = li.make_config(name)
+    if NATURAL and name != "C2":
+        raise SystemExit("--natural applies to C2")
+    m = li.make_config(name, natural=NATURAL)
     if QUAD8:
         if not (m.domain == li.SURFACE_TRI and m.order == 2):
             raise SystemExit("--quad8 applies to P2 triangle configs (C2, C5)")
@@ -185,7 +190,7 @@ def oracle_sample(m, kinds, coeff, target_s):
     """Time the oracle as it stands on a contiguous block of rows sized for
     about target_s seconds; returns (elements/s equivalent, rows, seconds, threads)."""
     import oracle
-    nt = os.cpu_count() or 1
+    nt = CPU_THREADS or os.cpu_count() or 1
     rows = _oracle_rows_for(m, kinds, coeff, target_s, nt)
     t0 = time.perf_counter()
     c = oracle.assemble_rows(m, kinds, rows=np.arange(rows, dtype=np.int64), coeff=coeff, nthreads=nt)
@@ -815,6 +820,34 @@ def run_lfem(args):
         step(t)
     prof = lfem.lfem_profile_read(plan)
     lfem.lfem_profile_enable(plan, False)
+    # --graph: the same numeric step captured once into a CUDA graph and replayed (SURVEY §8(d).6:
+    # launch overhead of the small configs); the graph's output is checked against the eager step
+    graph = None
+    if args.graph and u_work is None:
+        ref = [v.clone() if v is not None else None for v in vals]
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            lfem.lfem_assemble_numeric(plan, kmask, coeff, vals)
+        torch.cuda.synchronize()
+        for v in vals:
+            if v is not None:
+                v.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        same = all(torch.equal(a, b) for a, b in zip(vals, ref) if a is not None)
+        gev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        gs = torch.cuda.current_stream()
+        for t in range(args.steps):
+            if flush:
+                flush_buf.zero_()
+            gev[t][0].record(gs)
+            g.replay()
+            gev[t][1].record(gs)
+        torch.cuda.synchronize()
+        gms = sum(a.elapsed_time(b) for a, b in gev) / args.steps
+        graph = {"ms_per_step": gms, "value": n_elems / (gms * 1e-3), "eager_ms_per_step": None,
+                 "bitwise_equal_to_eager": bool(same), "note": "one CUDA-graph replay per step, events around each"}
+        del g
     clk = clocks.stop()
     evals, n_tiles = lfem.lfem_numeric_stats(plan)
 
@@ -961,6 +994,9 @@ def run_lfem(args):
                      "executed_tflops": FLOP_PER_ELEM[name] * evals / (step_kernel_ms * 1e-3) / 1e12},
             "clocks": clk, "e2e": e2e, "cpu_baseline": cpu, "verify": verify,
         }
+        if graph is not None:
+            graph["eager_ms_per_step"] = ms_per_step
+            line["graph"] = graph
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
@@ -976,6 +1012,10 @@ def main():
     ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "C4P1", "CURVE2"])
     ap.add_argument("--impl", default="lfem", choices=["lfem", "reference"])
     ap.add_argument("--variant", default="auto", choices=["auto", "v0", "tiled", "rows"])
+    ap.add_argument("--natural", action="store_true", help="C2 without the SFC renumbering (sensitivity point)")
+    ap.add_argument("--cpu-threads", type=int, default=None, help="threads of the oracle cpu_baseline sample")
+    ap.add_argument("--graph", action="store_true",
+                    help="also time the numeric step replayed from a captured CUDA graph (launch overhead)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -990,8 +1030,10 @@ def main():
     ap.add_argument("--rhs", default=None, choices=["load", "kll"],
                     help="time the right-hand side (SURVEY §8(f) N1) instead of the matrices")
     args = ap.parse_args()
-    global QUAD8
+    global QUAD8, NATURAL, CPU_THREADS
     QUAD8 = args.quad8
+    NATURAL = args.natural
+    CPU_THREADS = args.cpu_threads
     if args.warmup < 3:
         log("warmup raised to 3 (timing rules)")
         args.warmup = 3

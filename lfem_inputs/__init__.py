@@ -539,9 +539,11 @@ def displace_cube(x: np.ndarray, rng: SplitMix64) -> np.ndarray:
 CONFIG_NAMES = ("C1", "C2", "C3", "C4", "C5")  # BASELINE.json; "C4P1" = N2's P1 tets at scale
 
 
-def make_config(name: str, seed: int = 0, level_override: Optional[int] = None) -> Mesh:
+def make_config(name: str, seed: int = 0, level_override: Optional[int] = None, natural: bool = False) -> Mesh:
     """Build BASELINE.json configs[i] (C1..C5) as a Mesh.  `level_override`
-    builds the same recipe at a smaller size (tests only)."""
+    builds the same recipe at a smaller size (tests only).  `natural` keeps C2 in the
+    generator's own node / element numbering (the SURVEY §8(d).2 sensitivity point)
+    instead of the space-filling-curve order."""
     rng = SplitMix64(seed)
     if name == "C1":
         L = 3 if level_override is None else level_override
@@ -555,7 +557,8 @@ def make_config(name: str, seed: int = 0, level_override: Optional[int] = None) 
         L = 7 if level_override is None else level_override
         v, f = icosphere_p1(L)
         v, f = p2_from_p1_triangles(v, f, project_sphere=True)
-        v, f = sfc_reorder(v, f, 3)
+        if not natural:
+            v, f = sfc_reorder(v, f, 3)
         m = Mesh(SURFACE_TRI, 2, v, f, QUAD_TRI6_DEG4)
         m.extra["kinds"] = ("M", "A")
     elif name == "C3":
