@@ -125,6 +125,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
 #define LFEM_TILED_POISON 0
 #endif
 
+// Bounds mode (compile-time -DLFEM_BOUNDS=1, tests only; the stand-in for compute-sanitizer
+// memcheck, which this pool refuses): every shared-memory index of the tile kernel (node slots,
+// connectivity, stage positions and byte offsets, slot words, heavy entries), every bulk-copy
+// size against its buffer, every gathered global node id and every value store against the
+// tile's slot range is checked; a violation traps (the launch fails, the tests fail).
+#ifndef LFEM_BOUNDS
+#define LFEM_BOUNDS 0
+#endif
+#define LFEM_CHECK(cond)                    \
+    do {                                    \
+        if (LFEM_BOUNDS && !(cond)) __trap(); \
+    } while (0)
+
 // timing experiments only (compile-time, scripts/build_variants.py -DLFEM_TILED_SKIP=..):
 // bit0 compute warps skip the kind contractions, bit1 reduce warps skip the slots
 #ifndef LFEM_TILED_SKIP
@@ -198,7 +211,10 @@ extern __shared__ __align__(16) double tile_smem_d[];  // dynamic shared memory 
 struct StageSink {  // stage[s * maxe + e]
     double* st;
     int maxe, e;
-    __device__ __forceinline__ void operator()(int s, double v) const { st[s * maxe + e] = v; }
+    __device__ __forceinline__ void operator()(int s, double v) const {
+        LFEM_CHECK(e >= 0 && e < maxe);
+        st[s * maxe + e] = v;
+    }
 };
 
 // producer: publish tile t's info in sinfo[b] and start its bulk copies into meta buffer b
@@ -213,6 +229,9 @@ __device__ __forceinline__ void issue_tile(const TileArgs& a, unsigned char* sme
     const int h0 = i1.z & ~7, h1 = (i1.z + i1.w + 7) & ~7;    // u16, 16-B aligned
     const uint32_t bq = (uint32_t)i1.y * 2u, bp = (uint32_t)(p1 - p0) * 4u, bh = (uint32_t)(h1 - h0) * 2u;
     const uint32_t bl = (uint32_t)((i2.w + 3) & ~3) * 4u;     // halo list, 16-B padded per tile
+    LFEM_CHECK(lay.conn_off + bq <= lay.pairs_off && lay.pairs_off + bp <= lay.heavy_off &&
+               lay.heavy_off + bh <= lay.halo_off && lay.halo_off + bl <= lay.meta_bytes);
+    LFEM_CHECK(i0.w <= a.maxe && i0.y <= a.slots_cap && i2.y + 1 + i2.w <= a.nodes_cap + 1);
     fence_proxy_async();
     mbar_arrive_expect_tx(&bar[b], bq + bp + bh + bl);
     if (bq) bulk_g2s(buf + lay.conn_off, a.conn16 + i1.x, bq, &bar[b]);
@@ -268,6 +287,8 @@ __device__ __forceinline__ void prefetch_tile_nodes(const TileArgs& a, bool coef
     for (int h = tid; h < nh; h += ct) {
         const int64_t v = s_halo[h];
         const int l = nrows + 1 + h;
+        LFEM_CHECK(v >= 0 && v < a.n_nodes && o3 + 3 * l + 2 < (int)((lay.u_off) / sizeof(double)) &&
+                   o1 + l < (int)((lay.node_bytes - lay.u_off) / sizeof(double)));
 #pragma unroll
         for (int c = 0; c < 3; ++c) cp_async8(xyz + o3 + 3 * l + c, a.coords + 3 * v + c);
         if (coef) cp_async8(u + o1 + l, a.coeff + v);
@@ -289,6 +310,7 @@ __device__ __forceinline__ void read_nodes(const int4& i2, const uint16_t* s_con
 #pragma unroll
             for (int j = 0; j < N; ++j) {
                 const int l = s_conn[e * N + j];
+                LFEM_CHECK(l >= 0 && l < i2.y + 1 + i2.w && l != i2.y && e * N + j < (int)(lay.pairs_off / 2));
 #pragma unroll
                 for (int c = 0; c < 3; ++c) X[k][j][c] = xyz[3 * l + c];
                 U[k][j] = COEF ? u[l] : 0.0;
@@ -449,11 +471,15 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                     const uint4 w0 = ent[0];
                     const int cnt = (int)(w0.x >> 16);
                     slot = (int)(w0.x & 0xffffu);
+                    LFEM_CHECK(slot < ns && cnt > 2 && 6 + 8 * (hw / 8 - 1) >= cnt && (h + 1) * hw <= a.heavy_cap + 16);
                     const uint32_t c[6] = {w0.y & 0xffffu, w0.y >> 16, w0.z & 0xffffu, w0.z >> 16,
                                            w0.w & 0xffffu, w0.w >> 16};
                     double x[6];
 #pragma unroll
-                    for (int k = 0; k < 6; ++k) x[k] = *reinterpret_cast<const double*>(st + c[k]);
+                    for (int k = 0; k < 6; ++k) {
+                        LFEM_CHECK(c[k] % 8 == 0 && c[k] <= (uint32_t)tail_dbl * 8u);
+                        x[k] = *reinterpret_cast<const double*>(st + c[k]);
+                    }
                     double v = 0.0;
 #pragma unroll
                     for (int k = 0; k < 6; ++k) v = v + x[k];
@@ -463,8 +489,10 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                                                w.z & 0xffffu, w.z >> 16, w.w & 0xffffu, w.w >> 16};
                         double y[8];
 #pragma unroll
-                        for (int k = 0; k < 8; ++k)
+                        for (int k = 0; k < 8; ++k) {
+                            LFEM_CHECK(d[k] % 8 == 0 && d[k] <= (uint32_t)tail_dbl * 8u);
                             y[k] = *reinterpret_cast<const double*>(st + d[k]);
+                        }
 #pragma unroll
                         for (int k = 0; k < 8; ++k) v = v + y[k];
                     }
@@ -473,6 +501,8 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 auto slot_value = [&](uint32_t w) {
                     // x0 + x1 in the symbolic order (reading G21); for one contribution x1 = +0 (the
                     // oracle's 0 + x0: the same value, -0 becomes +0 in both)
+                    LFEM_CHECK((w & 7u) == 0 && (w & 0xffffu) <= (uint32_t)tail_dbl * 8u &&
+                               ((w >> 16) == 0xffffu || (w >> 16) <= (uint32_t)tail_dbl * 8u));
                     const double x0 = *reinterpret_cast<const double*>(st + (w & 0xffffu));
                     const uint32_t c1 = w >> 16;
                     const double x1 = (LFEM_ZERO_WORD || c1 != 0xffffu) ? *reinterpret_cast<const double*>(st + c1) : 0.0;
@@ -490,6 +520,7 @@ __global__ void __launch_bounds__((TileCfg<F>::CW + TileCfg<F>::RW) * 32, TileCf
                 }
 #pragma unroll RUN
                 for (int u = uA + rt; u < uB; u += RT) {
+                    LFEM_CHECK(2 * u - p0 + 1 < a.slots_cap + 8 && 2 * u >= s0 && 2 * u + 1 < se);
                     const uint2 w = *reinterpret_cast<const uint2*>(s_pw + (2 * u - p0));
                     const double v0 = slot_value(w.x), v1 = slot_value(w.y);
                     asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(out + 2 * u), "d"(v0), "d"(v1) : "memory");
