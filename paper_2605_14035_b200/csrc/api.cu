@@ -50,6 +50,8 @@ struct Profiler {
     }
 };
 
+bool prof_on(lfem_plan_s* p) { return p->prof && p->prof->on; }
+
 void prof_begin(lfem_plan_s* p, const char* name, cudaStream_t s) {
     if (!p->prof || !p->prof->on) return;
     Profiler& P = *p->prof;

@@ -77,11 +77,17 @@ struct TilePlan {
 struct McfWork {
     double *r = nullptr, *z = nullptr, *pv = nullptr, *q = nullptr, *b = nullptr, *dinv = nullptr;
     double *M = nullptr, *A = nullptr, *K = nullptr, *part = nullptr, *sc = nullptr;
+    // CUDA graph of CG_CHECK steady-state CG iterations (mcf.cu), keyed by the operands it captured
+    cudaGraphExec_t cg_exec = nullptr;
+    const double* cg_key_K = nullptr;
+    const double* cg_key_x = nullptr;
+    cudaStream_t cap = nullptr;  // private capture stream (the caller's may be the legacy stream)
     int* bad = nullptr;
 };
 struct Profiler;  // api.cu
 void prof_begin(lfem_plan_s* p, const char* name, cudaStream_t s);
 void prof_end(lfem_plan_s* p, cudaStream_t s);
+bool prof_on(lfem_plan_s* p);
 
 struct lfem_plan_s {
     lfem_mesh_s* mesh = nullptr;

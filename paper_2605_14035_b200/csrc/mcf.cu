@@ -227,6 +227,8 @@ static lfem_status mcf_work(lfem_plan_s* p, cudaStream_t s) {
 
 void mcf_free(lfem_plan_s* p, cudaStream_t s) {
     McfWork& W = p->mcf;
+    if (W.cg_exec) cudaGraphExecDestroy(W.cg_exec);
+    if (W.cap) cudaStreamDestroy(W.cap);
     for (void* v : {(void*)W.r, (void*)W.z, (void*)W.pv, (void*)W.q, (void*)W.b, (void*)W.dinv, (void*)W.M,
                     (void*)W.A, (void*)W.K, (void*)W.part, (void*)W.sc, (void*)W.bad})
         dev_free(v, s);
@@ -280,18 +282,53 @@ static lfem_status cg_run(lfem_plan_s* p, const double* vals_K, const double* b,
             if (done) return LFEM_OK;
             if (it >= max_it) return lfem_fail(LFEM_ERR_STATE, "CG did not converge within max_it iterations");
         }
-        if (it > 0) {  // p = z + beta p with beta = rz_new / rz, rz <- rz_new
-            k_cg_dir<<<grid_rows(n, 256), 256, 0, s>>>(n, S + 9, S, W.z, W.pv);
-            k_copy_rz<<<1, 32, 0, s>>>(S + 9, S);
+        // one iteration: p = z + beta p (beta = rz_new / rz, rz <- rz_new; not in the first), q = K p,
+        // alpha = rz / pq, x += alpha p, r -= alpha q, z = D^-1 r, rz_new, rr_new
+        auto body = [&](cudaStream_t st, bool first) -> lfem_status {
+            if (!first) {
+                k_cg_dir<<<grid_rows(n, 256), 256, 0, st>>>(n, S + 9, S, W.z, W.pv);
+                k_copy_rz<<<1, 32, 0, st>>>(S + 9, S);
+            }
+            prof_begin(p, "k_spmm3", st);
+            k_spmm3<<<gsp, 256, 0, st>>>(n, p->row_ptr, p->col_idx, vals_K, W.pv, W.q);
+            prof_end(p, st);
+            k_dot_pq<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(n, W.pv, W.q, W.part);
+            k_final<3><<<1, 32, 0, st>>>(W.part, DOT_BLOCKS, S + 6);
+            k_cg_update<<<DOT_BLOCKS, DOT_THREADS, 0, st>>>(n, S, W.pv, W.q, W.dinv, x, W.r, W.z, W.part);
+            k_final<6><<<1, 32, 0, st>>>(W.part, DOT_BLOCKS, S + 9);
+            LFEM_CUDA(cudaGetLastError());
+            return LFEM_OK;
+        };
+        // steady state: CG_CHECK iterations (7 launches each) replayed from one captured CUDA graph
+        // (the same kernels in the same order: the same bits); per-kernel profiling runs them eagerly
+        if (it > 0 && it % CG_CHECK == 0 && it + CG_CHECK <= max_it && !prof_on(p)) {
+            if (!W.cg_exec || W.cg_key_K != vals_K || W.cg_key_x != x) {
+                if (W.cg_exec) {
+                    cudaGraphExecDestroy(W.cg_exec);
+                    W.cg_exec = nullptr;
+                }
+                if (!W.cap) LFEM_CUDA(cudaStreamCreateWithFlags(&W.cap, cudaStreamNonBlocking));
+                cudaGraph_t g = nullptr;
+                LFEM_CUDA(cudaStreamBeginCapture(W.cap, cudaStreamCaptureModeThreadLocal));
+                lfem_status st = LFEM_OK;
+                for (int k = 0; k < CG_CHECK && st == LFEM_OK; ++k) st = body(W.cap, false);
+                const cudaError_t ec = cudaStreamEndCapture(W.cap, &g);
+                if (st != LFEM_OK) {
+                    if (g) cudaGraphDestroy(g);
+                    return st;
+                }
+                LFEM_CUDA(ec);
+                const cudaError_t ei = cudaGraphInstantiate(&W.cg_exec, g, 0);
+                cudaGraphDestroy(g);
+                LFEM_CUDA(ei);
+                W.cg_key_K = vals_K;
+                W.cg_key_x = x;
+            }
+            LFEM_CUDA(cudaGraphLaunch(W.cg_exec, s));
+            it += CG_CHECK - 1;
+            continue;
         }
-        prof_begin(p, "k_spmm3", s);
-        k_spmm3<<<gsp, 256, 0, s>>>(n, p->row_ptr, p->col_idx, vals_K, W.pv, W.q);
-        prof_end(p, s);
-        k_dot_pq<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, W.pv, W.q, W.part);
-        k_final<3><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 6);
-        k_cg_update<<<DOT_BLOCKS, DOT_THREADS, 0, s>>>(n, S, W.pv, W.q, W.dinv, x, W.r, W.z, W.part);
-        k_final<6><<<1, 32, 0, s>>>(W.part, DOT_BLOCKS, S + 9);
-        LFEM_CUDA(cudaGetLastError());
+        LFEM_TRY(body(s, it == 0));
     }
 }
 
