@@ -1,7 +1,9 @@
 """GPU parity at BASELINE.json's full sizes (C2..C5), in the launch
 configuration bench.py times: sampled rows against the oracle (computed row
-by row), plus properties that hold at any size (A 1 = 0, 1^T M 1, trace
-identities) evaluated with the library's own SpMV over every row."""
+by row), properties that hold at any size (A 1 = 0, 1^T M 1, trace
+identities) evaluated with the library's own SpMV over every row, and (round 2)
+EVERY row of C3, C4 and C5 against the oracle, block by block (C5: 41.9M rows,
+3 x 482M values; ~2 min on the GPU box's 16 host cores)."""
 import math
 
 import numpy as np
@@ -50,6 +52,36 @@ def _check_sampled(m, kinds, row_ptr, col_idx, vals, coeff, nsample=1500):
             scale = np.abs(ov).max()
             assert err <= TOL * scale, (k, rows[j], err, scale)
             worst = max(worst, err / scale)
+    return worst
+
+
+def _check_every_row(m, kinds, row_ptr, col_idx, vals, coeff, block=1 << 21):
+    """Every row of the full-size assembly against the oracle, block by block (bounded host
+    memory): pattern bit-exact, every value within TOL x its row's max |oracle entry|."""
+    rp = row_ptr.cpu().numpy()
+    worst = 0.0
+    for r0 in range(0, m.n_nodes, block):
+        r1 = min(m.n_nodes, r0 + block)
+        o = oracle.assemble_rows(m, kinds, rows=np.arange(r0, r1, dtype=np.int64), coeff=coeff)
+        s0, s1 = int(rp[r0]), int(rp[r1])
+        assert np.array_equal(rp[r0:r1 + 1] - s0, o.row_ptr), f"row_ptr mismatch in rows [{r0}, {r1})"
+        assert np.array_equal(col_idx[s0:s1].cpu().numpy(), o.col_idx), f"col_idx mismatch in rows [{r0}, {r1})"
+        lens = np.diff(o.row_ptr)
+        nz = lens > 0
+        row_of = np.repeat(np.arange(r1 - r0), lens)
+        for k in kinds:
+            ov = o.vals[k]
+            gv = vals[k][s0:s1].cpu().numpy()
+            rowmax = np.zeros(r1 - r0)
+            rowmax[nz] = np.maximum.reduceat(np.abs(ov), o.row_ptr[:-1][nz])
+            err = np.abs(gv - ov)
+            scale = rowmax[row_of]
+            bad = err > TOL * scale
+            assert not bad.any(), (k, int(r0 + row_of[np.argmax(bad)]), float(err[bad].max()))
+            with np.errstate(divide="ignore", invalid="ignore"):
+                rel = np.where(scale > 0, err / scale, 0.0)
+            worst = max(worst, float(rel.max()) if rel.size else 0.0)
+        del o
     return worst
 
 
@@ -133,3 +165,13 @@ def test_C5_full():
     _check_sampled(m, kinds, rp, ci, vals, m.coeff)
     mass = _properties(m, kinds, plan, vals, m.coeff, 2)
     assert abs(mass - 4 * math.pi) < 1e-9
+
+
+# Every row at full size, in bench.py's launch configuration (AUTO: TILED for C3 / C5, V0 for C4)
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_every_row(name):
+    m = li.make_config(name)
+    coeff = m.coeff
+    m2, kinds, plan, rp, ci, vals = m, KINDS[name], *lfem.assemble(m, KINDS[name], coeff=coeff)
+    worst = _check_every_row(m2, kinds, rp, ci, vals, coeff)
+    assert worst <= TOL
