@@ -215,6 +215,17 @@ def test_rhs_fullsize_sampled(cfg, kind):
     check(out[:, torch.as_tensor(rows, device="cuda")].cpu().numpy(), o, oabs)
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,kind", [("C5", "kll"), ("C4", "load")])
+def test_rhs_fullsize_every_row(cfg, kind):
+    """BASELINE.json full sizes, EVERY row against the oracle (the oracle over all rows at once)."""
+    m = li.make_config(cfg)
+    u = fields(m, kind, seed=9)
+    _, out = lfem.assemble_rhs(m, u, kind)
+    o, oabs = oracle.assemble_rhs_rows(m, u, kind, with_abs=True)
+    check(out.cpu().numpy(), o, oabs)
+
+
 @pytest.mark.parametrize("variant", VARIANTS, ids=["v0", "fused"])
 def test_rhs_empty_row_block_and_tiny_mesh(variant):
     """Degenerate sizes: an empty owned-row block, a one-row block, and a single element."""
