@@ -34,9 +34,17 @@
 #ifndef LFEM_P1_EPT
 #define LFEM_P1_EPT 4
 #endif
-#ifndef LFEM_P1_REGS_C  // P1 triangles (C3): register split measured best in round 1
-#define LFEM_P1_REGS_C 176
-#define LFEM_P1_REGS_R 80
+// P1 triangles (C3): CTA shape (compute warps, reduce warps) and register split; 8 + 8 warps at
+// 176 / 80 registers measured best (DESIGN.md §6.3 lists the shapes measured slower)
+#ifndef LFEM_P1_CW
+#define LFEM_P1_CW 8
+#endif
+#ifndef LFEM_P1_RW
+#define LFEM_P1_RW LFEM_RW
+#endif
+#ifndef LFEM_P1_REGS_C
+#define LFEM_P1_REGS_C (LFEM_P1_RW == 8 && LFEM_P1_CW == 8 ? 176 : 0)
+#define LFEM_P1_REGS_R (LFEM_P1_RW == 8 && LFEM_P1_CW == 8 ? 80 : 0)
 #endif
 // P2 triangles: CTA shape (compute warps, reduce warps, CTAs per SM, elements per compute thread)
 #ifndef LFEM_P2_CW
@@ -152,7 +160,7 @@ __device__ __forceinline__ void st_stream(double* p, double v) {
 // element budget CW*32*EPT), REGS_C / REGS_R setmaxnreg budgets of the two
 // roles (0 = launch default).
 template <int F> struct TileCfg;
-template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = 8, RW = LFEM_RW, EPT = LFEM_P1_EPT, MINB = 1, REGS_C = LFEM_RW == 8 ? LFEM_P1_REGS_C : 0, REGS_R = LFEM_RW == 8 ? LFEM_P1_REGS_R : 0; };
+template <> struct TileCfg<FAM_TRI_P1> { static constexpr int CW = LFEM_P1_CW, RW = LFEM_P1_RW, EPT = LFEM_P1_EPT, MINB = 1, REGS_C = LFEM_P1_REGS_C, REGS_R = LFEM_P1_REGS_R; };
 template <> struct TileCfg<FAM_TRI_P2> { static constexpr int CW = LFEM_P2_CW, RW = LFEM_P2_RW, MINB = LFEM_P2_MINB, EPT = LFEM_P2_EPT, REGS_C = LFEM_REGS_C, REGS_R = LFEM_REGS_R; };
 template <> struct TileCfg<FAM_TRI_P2_Q16> : TileCfg<FAM_TRI_P2> {};
 template <> struct TileCfg<FAM_TET_P1> { static constexpr int CW = 8, RW = 4, MINB = 1, EPT = 1, REGS_C = 0, REGS_R = 0; };
