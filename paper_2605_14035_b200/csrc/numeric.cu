@@ -112,59 +112,117 @@ k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __r
 }
 
 // thread per CSR slot; contributions in plan order (ascending element, then (a, b): G21)
+// LFEM_V0_KS > 1: each thread owns KS slots (blockDim apart, so the warp's
+// accesses stay coalesced); the first two contributions of all KS slots are loaded together
+// (2 KS independent gathers in flight per thread: most P2 slots have <= 2 contributions),
+// the rest of each slot in the usual loops.  The order within a slot is unchanged.
+#ifndef LFEM_V0_KS
+#define LFEM_V0_KS 2
+#endif
 template <bool DM, bool DA, bool DAA>
 __global__ void __launch_bounds__(256)
 k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* __restrict__ codes,
               const double* __restrict__ stage, double* __restrict__ vm, double* __restrict__ va,
               double* __restrict__ vaa) {
     constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
-    for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nnz; s += (int64_t)gridDim.x * blockDim.x) {
-        const int j0 = __ldg(&slot_ptr[s]), j1 = __ldg(&slot_ptr[s + 1]);
-        double acc[NK];
+    constexpr int KS = LFEM_V0_KS;
+    const int64_t per_block = (int64_t)blockDim.x * KS;
+    for (int64_t base = blockIdx.x * per_block + threadIdx.x; base < nnz; base += (int64_t)gridDim.x * per_block) {
+        int jb[KS], je[KS];
+        double acc[KS][NK];
 #pragma unroll
-        for (int k = 0; k < NK; ++k) acc[k] = 0.0;
-        // four contributions' loads in flight, accumulated in plan order
-        int j = j0;
-        for (; j + 4 <= j1; j += 4) {
-            int c4[4];
+        for (int q = 0; q < KS; ++q) {
+            const int64_t s = base + (int64_t)q * blockDim.x;
+            jb[q] = je[q] = 0;
+            if (s < nnz) {
+                jb[q] = __ldg(&slot_ptr[s]);
+                je[q] = __ldg(&slot_ptr[s + 1]);
+            }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) c4[u] = __ldg(&codes[j + u]);
-            if constexpr (NK == 2) {
-                double2 w4[4];
+            for (int k = 0; k < NK; ++k) acc[q][k] = 0.0;
+        }
+        if constexpr (KS > 1) {
+            int c2[KS][2];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) w4[u] = __ldg(reinterpret_cast<const double2*>(stage + (int64_t)c4[u] * 2));
+            for (int q = 0; q < KS; ++q)
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    acc[0] += w4[u].x;
-                    acc[1] += w4[u].y;
+                for (int u = 0; u < 2; ++u) c2[q][u] = (jb[q] + u < je[q]) ? __ldg(&codes[jb[q] + u]) : -1;
+            double w2[KS][2][NK];
+#pragma unroll
+            for (int q = 0; q < KS; ++q)
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    if constexpr (NK == 2) {
+                        double2 w = make_double2(0.0, 0.0);
+                        if (c2[q][u] >= 0) w = __ldg(reinterpret_cast<const double2*>(stage + (int64_t)c2[q][u] * 2));
+                        w2[q][u][0] = w.x;
+                        w2[q][u][1] = w.y;
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < NK; ++k)
+                            w2[q][u][k] = c2[q][u] >= 0 ? __ldg(stage + (int64_t)c2[q][u] * NK + k) : 0.0;
+                    }
                 }
-            } else {
-                double w4[4][NK];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
+            for (int q = 0; q < KS; ++q) {
 #pragma unroll
-                    for (int k = 0; k < NK; ++k) w4[u][k] = __ldg(stage + (int64_t)c4[u] * NK + k);
+                for (int u = 0; u < 2; ++u)
+                    if (c2[q][u] >= 0) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-#pragma unroll
-                    for (int k = 0; k < NK; ++k) acc[k] += w4[u][k];
+                        for (int k = 0; k < NK; ++k) acc[q][k] += w2[q][u][k];
+                    }
+                jb[q] = min(jb[q] + 2, je[q]);
             }
         }
-        for (; j < j1; ++j) {
-            const double* p = stage + (int64_t)__ldg(&codes[j]) * NK;
-            if constexpr (NK == 2) {
-                const double2 w = __ldg(reinterpret_cast<const double2*>(p));
-                acc[0] += w.x;
-                acc[1] += w.y;
-            } else {
 #pragma unroll
-                for (int k = 0; k < NK; ++k) acc[k] += __ldg(p + k);
+        for (int q = 0; q < KS; ++q) {
+            const int j1 = je[q];
+            // four contributions' loads in flight, accumulated in plan order
+            int j = jb[q];
+            for (; j + 4 <= j1; j += 4) {
+                int c4[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) c4[u] = __ldg(&codes[j + u]);
+                if constexpr (NK == 2) {
+                    double2 w4[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) w4[u] = __ldg(reinterpret_cast<const double2*>(stage + (int64_t)c4[u] * 2));
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        acc[q][0] += w4[u].x;
+                        acc[q][1] += w4[u].y;
+                    }
+                } else {
+                    double w4[4][NK];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < NK; ++k) w4[u][k] = __ldg(stage + (int64_t)c4[u] * NK + k);
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+#pragma unroll
+                        for (int k = 0; k < NK; ++k) acc[q][k] += w4[u][k];
+                }
+            }
+            for (; j < j1; ++j) {
+                const double* p = stage + (int64_t)__ldg(&codes[j]) * NK;
+                if constexpr (NK == 2) {
+                    const double2 w = __ldg(reinterpret_cast<const double2*>(p));
+                    acc[q][0] += w.x;
+                    acc[q][1] += w.y;
+                } else {
+#pragma unroll
+                    for (int k = 0; k < NK; ++k) acc[q][k] += __ldg(p + k);
+                }
+            }
+            const int64_t s = base + (int64_t)q * blockDim.x;
+            if (s < nnz) {
+                int kr = 0;
+                if (DM) vm[s] = acc[q][kr++];
+                if (DA) va[s] = acc[q][kr++];
+                if (DAA) vaa[s] = acc[q][kr++];
             }
         }
-        int kr = 0;
-        if (DM) vm[s] = acc[kr++];
-        if (DA) va[s] = acc[kr++];
-        if (DAA) vaa[s] = acc[kr++];
     }
 }
 
@@ -191,7 +249,7 @@ lfem_status run_v0(lfem_plan_s* p, const double* coords, const double* coeff, do
     }
     if (p->nnz > 0) {
         prof_begin(p, "k_slot_reduce", s);
-        k_slot_reduce<DM, DA, DAA><<<grid_for(p->nnz, 256, 1 << 20), 256, 0, s>>>(
+        k_slot_reduce<DM, DA, DAA><<<grid_for(p->nnz, 256 * LFEM_V0_KS, 1 << 20), 256, 0, s>>>(
             p->nnz, p->slot_ptr, p->codes, p->stage, vals[0], vals[1], vals[2]);
         LFEM_CUDA(cudaGetLastError());
         prof_end(p, s);
