@@ -113,11 +113,16 @@ k_elem_v0(int64_t n_local, const int32_t* __restrict__ lconn, const int32_t* __r
 
 // thread per CSR slot; contributions in plan order (ascending element, then (a, b): G21)
 // LFEM_V0_KS > 1: each thread owns KS slots (blockDim apart, so the warp's
-// accesses stay coalesced); the first two contributions of all KS slots are loaded together
-// (2 KS independent gathers in flight per thread: most P2 slots have <= 2 contributions),
-// the rest of each slot in the usual loops.  The order within a slot is unchanged.
+// accesses stay coalesced); the first LFEM_V0_U2 contributions of all KS slots are loaded
+// together, predicated (KS * U2 independent gathers in flight per thread: most slots have
+// <= 4 contributions), the rest of each slot in the usual loops.  The order within a slot
+// is unchanged.  Measured (C4 reduce, ms): KS,U2 = 1,- 2.89 | 2,2 2.85 | 2,4 2.67 | 2,3 3.08
+// | 2,6 3.49 | 2,8 3.00 | 3,2 3.12 | 4,2 3.22.
 #ifndef LFEM_V0_KS
 #define LFEM_V0_KS 2
+#endif
+#ifndef LFEM_V0_U2
+#define LFEM_V0_U2 4
 #endif
 template <bool DM, bool DA, bool DAA>
 __global__ void __launch_bounds__(256)
@@ -126,6 +131,7 @@ k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* 
               double* __restrict__ vaa) {
     constexpr int NK = (DM ? 1 : 0) + (DA ? 1 : 0) + (DAA ? 1 : 0);
     constexpr int KS = LFEM_V0_KS;
+    [[maybe_unused]] constexpr int U2 = LFEM_V0_U2;  // contributions per slot gathered in the joint first round
     const int64_t per_block = (int64_t)blockDim.x * KS;
     for (int64_t base = blockIdx.x * per_block + threadIdx.x; base < nnz; base += (int64_t)gridDim.x * per_block) {
         int jb[KS], je[KS];
@@ -142,16 +148,16 @@ k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* 
             for (int k = 0; k < NK; ++k) acc[q][k] = 0.0;
         }
         if constexpr (KS > 1) {
-            int c2[KS][2];
+            int c2[KS][U2];
 #pragma unroll
             for (int q = 0; q < KS; ++q)
 #pragma unroll
-                for (int u = 0; u < 2; ++u) c2[q][u] = (jb[q] + u < je[q]) ? __ldg(&codes[jb[q] + u]) : -1;
-            double w2[KS][2][NK];
+                for (int u = 0; u < U2; ++u) c2[q][u] = (jb[q] + u < je[q]) ? __ldg(&codes[jb[q] + u]) : -1;
+            double w2[KS][U2][NK];
 #pragma unroll
             for (int q = 0; q < KS; ++q)
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
+                for (int u = 0; u < U2; ++u) {
                     if constexpr (NK == 2) {
                         double2 w = make_double2(0.0, 0.0);
                         if (c2[q][u] >= 0) w = __ldg(reinterpret_cast<const double2*>(stage + (int64_t)c2[q][u] * 2));
@@ -166,12 +172,12 @@ k_slot_reduce(int64_t nnz, const int32_t* __restrict__ slot_ptr, const int32_t* 
 #pragma unroll
             for (int q = 0; q < KS; ++q) {
 #pragma unroll
-                for (int u = 0; u < 2; ++u)
+                for (int u = 0; u < U2; ++u)
                     if (c2[q][u] >= 0) {
 #pragma unroll
                         for (int k = 0; k < NK; ++k) acc[q][k] += w2[q][u][k];
                     }
-                jb[q] = min(jb[q] + 2, je[q]);
+                jb[q] = min(jb[q] + U2, je[q]);
             }
         }
 #pragma unroll
